@@ -1,0 +1,169 @@
+/*
+ * phgrms_b200.h -- C ABI of the B200-native P-HGRMS denoise path.
+ *
+ * The reference (arXiv 1306.5390 artifact, /root/reference/proj) has no FFI:
+ * its boundary is the header-only C++ API in include/phgrms/denoise.hpp.
+ * Every entry point below replaces one piece of that API; the C++ drop-in
+ * headers in include/phgrms/ (same names and signatures as the reference)
+ * are thin wrappers over these symbols, and INTEGRATION.md shows the
+ * bindings a maintainer would add.
+ *
+ * Conventions
+ *   - Images are uint8, row-major, index r*width+c, unpadded on the host
+ *     side (reference: include/phgrms/image.hpp:16-51).
+ *   - Every function returns PHG_OK (0) or a negative PHG_E* code; the
+ *     message of the last failure on the calling thread is phg_last_error().
+ *     PHG_EINVAL carries the reference's exact std::invalid_argument text.
+ *   - Host-buffer functions are synchronous and blocking, like the
+ *     reference; they run on the calling thread's current device (set with
+ *     phg_set_device) on a library-owned stream.
+ *   - Device functions (phg_dev_*) take device pointers and a cudaStream_t
+ *     passed as void*; they enqueue work and return without synchronising.
+ *   - There is no CPU fallback: without a usable CUDA device every compute
+ *     entry point fails with PHG_ENODEV.
+ */
+#ifndef PHGRMS_B200_H
+#define PHGRMS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PHG_ABI_VERSION 1
+
+enum {
+    PHG_OK = 0,
+    PHG_EINVAL = -1, /* std::invalid_argument in the reference            */
+    PHG_ECUDA = -2,  /* CUDA runtime / driver failure                      */
+    PHG_ENOMEM = -3, /* device or host allocation failure                  */
+    PHG_ENODEV = -4  /* no usable CUDA device / kernel image               */
+};
+
+/* BorderMode, include/phgrms/denoise.hpp:27-30 */
+enum { PHG_BORDER_FAITHFUL = 0, PHG_BORDER_INBOUNDS = 1 };
+
+/* DenoiseParams, include/phgrms/denoise.hpp:34-52 (same field order). */
+typedef struct phg_params {
+    int32_t alpha;          /* |a-b| < alpha, alpha in [1,255]              */
+    int32_t beta;           /* window radius >= 1                          */
+    int32_t max_iterations; /* iteration cap k >= 1                        */
+    int32_t card_threshold; /* flagged when cardinality < threshold, >= 1  */
+    int32_t border;         /* PHG_BORDER_*                                */
+} phg_params;
+
+/* PassStats, include/phgrms/denoise.hpp:71-76 (same layout). */
+typedef struct phg_pass_stats {
+    int32_t iteration; /* 1-based */
+    int32_t _pad;
+    int64_t flagged;
+    int64_t replaced;
+    double elapsed_ms;
+} phg_pass_stats;
+
+/* ---------------------------------------------------------------- misc */
+int phg_abi_version(void);
+const char* phg_last_error(void);
+/* DenoiseParams::validate (denoise.hpp:41-49): PHG_OK or PHG_EINVAL. */
+int phg_validate_params(const phg_params* p);
+int phg_device_count(int* count);
+int phg_set_device(int device);
+/* Kernel launches issued by this library on the calling thread since the
+ * last reset (evidence for bench.py's gpu_launches). */
+int64_t phg_launch_count(void);
+void phg_reset_launch_count(void);
+
+/* -------------------------------------------- reference API, host buffers */
+
+/* compute_cardinality (denoise.hpp:227-241): counts[r*w+c] = number of
+ * in-bounds window cells alpha-similar to (r,c), centre included. */
+int phg_cardinality(const uint8_t* img, int width, int height, int alpha, int beta,
+                    int32_t* counts);
+
+/* denoise_pass (denoise.hpp:243-283) with a caller-supplied cardinality map
+ * of card_width x card_height; writes a fresh image to `out` and one
+ * PassStats (iteration = 1). */
+int phg_denoise_pass(const uint8_t* img, int width, int height, const int32_t* card,
+                     int card_width, int card_height, const phg_params* p, uint8_t* out,
+                     phg_pass_stats* stats);
+
+/* denoise (denoise.hpp:292-311): iterate up to p->max_iterations, stop
+ * after the first iteration that replaced nothing.  `stats` has capacity
+ * p->max_iterations; *iterations_run entries are filled.  bands >= 2 runs
+ * the row-band sharded engine (the reference's Parallel engine, row_blocks
+ * partition, denoise.hpp:97-107) with halo exchange between bands on one
+ * device; results are bit-identical for every band count. */
+int phg_denoise(const uint8_t* img, int width, int height, const phg_params* p, int bands,
+                uint8_t* out, phg_pass_stats* stats, int* iterations_run);
+
+/* Batch of n independent images packed [n][height][width]; stats is
+ * [n][max_iterations], iterations_run is [n]. */
+int phg_denoise_batch(const uint8_t* imgs, int n, int width, int height, const phg_params* p,
+                      uint8_t* out, phg_pass_stats* stats, int* iterations_run);
+
+/* Input generators restated from the reference (out of the hot path; used
+ * to build bench inputs without the oracle): synth_image(SmoothRandom=2,
+ * Gradient=0, Checker=1), image.hpp:53-106; inject_sp_noise, noise.hpp:62-89
+ * (mask may be NULL; returns corrupted count or PHG_EINVAL). */
+int phg_synth_image(int width, int height, uint32_t seed, int kind, uint8_t* out);
+int64_t phg_inject_sp_noise(const uint8_t* img, int width, int height, double density,
+                            double salt_ratio, uint32_t seed, uint8_t* out, uint8_t* mask);
+
+/* ------------------------------------- device-resident API (HBM inputs) */
+
+/* A pitched device layout: image i, row r, column c lives at
+ * data + i*image_stride + r*pitch + c.  pitch and image_stride must be
+ * multiples of 16 (TMA), data 16-byte aligned. */
+typedef struct phg_dev_image {
+    uint8_t* data;
+    int64_t pitch;
+    int64_t image_stride;
+    int32_t width;
+    int32_t rows; /* rows held by the buffer (band rows incl. halo, or height) */
+    int32_t n_images;
+    int32_t _pad;
+} phg_dev_image;
+
+/* Largest number of iterations one fused launch can take for this beta
+ * (temporal blocking depth; 0 if beta has no fused kernel). */
+int phg_max_fused_iterations(int beta);
+
+/* One temporally blocked launch: `iters` (1..phg_max_fused_iterations)
+ * fused cardinality+removal iterations, reading `src` and writing `dst`
+ * (same geometry).  Buffer row y is global image row y + row_base of an
+ * image with `height` rows; only global rows [own_lo, own_hi) are written
+ * to dst and counted, and src must hold valid data for global rows
+ * [own_lo - beta*iters, own_hi + beta*iters) clipped to [0, height).
+ * counters (device, uint64 [n_images][kcap][2] = flagged, replaced) are
+ * accumulated at iteration index it0 .. it0+iters-1. */
+int phg_dev_fused_step(const phg_dev_image* src, const phg_dev_image* dst, int row_base,
+                       int height, int own_lo, int own_hi, const phg_params* p, int it0,
+                       int iters, uint64_t* counters, int kcap, void* stream);
+
+/* Full k-iteration denoise of whole images resident on the device:
+ * reads src, leaves the result in dst, uses tmp as the ping-pong partner
+ * (src is never written, so the call is repeatable).  counters as above
+ * with kcap = p->max_iterations, zeroed by the call. */
+int phg_dev_denoise(const phg_dev_image* src, const phg_dev_image* dst,
+                    const phg_dev_image* tmp, const phg_params* p, uint64_t* counters,
+                    void* stream);
+
+/* Standalone passes on device buffers (cardinality int32 pitched by
+ * card_pitch elements). */
+int phg_dev_cardinality(const phg_dev_image* src, int alpha, int beta, int32_t* card,
+                        int64_t card_pitch, void* stream);
+int phg_dev_removal(const phg_dev_image* src, const int32_t* card, int64_t card_pitch,
+                    const phg_params* p, const phg_dev_image* dst, uint64_t* counters,
+                    void* stream);
+
+/* Turn device counters into reference PassStats: per image, truncate after
+ * the first iteration with replaced == 0 (denoise.hpp:308). */
+int phg_finalize_stats(const uint64_t* host_counters, int n_images, int kcap,
+                       phg_pass_stats* stats, int* iterations_run);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PHGRMS_B200_H */

@@ -1,0 +1,30 @@
+"""B200-native P-HGRMS (arXiv 1306.5390) denoise path.
+
+The C++ reference API (include/phgrms/denoise.hpp) re-served from sm_100a
+kernels through the C ABI in include/phgrms_b200.h.  See DESIGN.md.
+"""
+from ._lib import LIB_PATH, CudaError, InvalidArgument, lib  # noqa: F401
+from .phgrms import (  # noqa: F401
+    BorderMode,
+    CardinalityMap,
+    DenoiseParams,
+    DenoiseResult,
+    EngineMode,
+    EngineSpec,
+    GrayImage,
+    NoiseSpec,
+    PassStats,
+    RowBlock,
+    SynthKind,
+    compute_cardinality,
+    denoise,
+    denoise_batch,
+    denoise_pass,
+    inject_sp_noise,
+    parallel_for_rows,
+    residual_noise_count,
+    rms_replacement,
+    row_blocks,
+    similar,
+    synth_image,
+)

@@ -1,0 +1,693 @@
+// phgrms_cuda.cu -- host side of the B200-native P-HGRMS path: the C ABI of
+// include/phgrms_b200.h over the kernels in kernels.cuh.
+//
+// Reference interfaces replaced (paths relative to /root/reference/proj):
+//   compute_cardinality  include/phgrms/denoise.hpp:227-241 -> phg_cardinality
+//   denoise_pass         include/phgrms/denoise.hpp:243-283 -> phg_denoise_pass
+//   denoise              include/phgrms/denoise.hpp:292-311 -> phg_denoise
+//   Parallel engine      include/phgrms/denoise.hpp:97-135  -> phg_denoise(bands)
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "../../include/phgrms_b200.h"
+#include "kernels.cuh"
+
+namespace {
+
+thread_local std::string g_error;
+thread_local int64_t g_launches = 0;
+
+int fail(int code, const std::string& msg) {
+    g_error = msg;
+    return code;
+}
+
+#define PHG_CUDA(expr)                                                                      \
+    do {                                                                                    \
+        cudaError_t e_ = (expr);                                                            \
+        if (e_ != cudaSuccess)                                                              \
+            return fail(e_ == cudaErrorMemoryAllocation ? PHG_ENOMEM                        \
+                        : (e_ == cudaErrorNoDevice || e_ == cudaErrorInsufficientDriver ||  \
+                           e_ == cudaErrorNoKernelImageForDevice)                           \
+                            ? PHG_ENODEV                                                    \
+                            : PHG_ECUDA,                                                    \
+                        std::string(#expr) + ": " + cudaGetErrorString(e_));                \
+    } while (0)
+
+#define PHG_TRY(expr)              \
+    do {                           \
+        int rc_ = (expr);          \
+        if (rc_ != PHG_OK) return rc_; \
+    } while (0)
+
+// Exact messages of DenoiseParams::validate (denoise.hpp:41-49).
+int validate(const phg_params* p) {
+    if (!p) return fail(PHG_EINVAL, "null params");
+    if (p->alpha < 1 || p->alpha > 255) return fail(PHG_EINVAL, "alpha must be in [1, 255]");
+    if (p->beta < 1) return fail(PHG_EINVAL, "beta must be >= 1");
+    if (p->max_iterations < 1) return fail(PHG_EINVAL, "iterations must be >= 1");
+    if (p->card_threshold < 1) return fail(PHG_EINVAL, "card_threshold must be >= 1");
+    if (p->border != PHG_BORDER_FAITHFUL && p->border != PHG_BORDER_INBOUNDS)
+        return fail(PHG_EINVAL, "border must be Faithful or InBounds");
+    return PHG_OK;
+}
+
+int check_dims(int w, int h) {
+    // GrayImage ctor (image.hpp:24-34)
+    if (w < 1 || h < 1) return fail(PHG_EINVAL, "image dimensions must be >= 1");
+    return PHG_OK;
+}
+
+int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+// ---------------------------------------------------------- TMA encoding
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_encode_once;
+
+int encode_map(CUtensorMap* map, const phg_dev_image& im, int box_cols, int box_rows) {
+    std::call_once(g_encode_once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    });
+    if (!g_encode) return fail(PHG_ENODEV, "cuTensorMapEncodeTiled unavailable");
+    if ((reinterpret_cast<uintptr_t>(im.data) & 15) || (im.pitch & 15) || (im.image_stride & 15))
+        return fail(PHG_EINVAL, "device image must be 16-byte aligned with 16-byte pitches");
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(im.width), static_cast<cuuint64_t>(im.rows),
+                          static_cast<cuuint64_t>(im.n_images)};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(im.pitch),
+                             static_cast<cuuint64_t>(im.n_images > 1 ? im.image_stride
+                                                                     : im.pitch * im.rows)};
+    if (strides[1] == 0) strides[1] = 16;
+    cuuint32_t box[3] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows), 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, im.data, dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(PHG_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+    return PHG_OK;
+}
+
+// ------------------------------------------------------ kernel dispatch
+using FusedFn = void (*)(const CUtensorMap, const CUtensorMap, const phg::TileArgs);
+
+template <int B, int T, bool A>
+FusedFn fused_ptr() {
+    return phg::fused_tb_kernel<B, T, A>;
+}
+
+FusedFn select_fused(int beta, int T, bool ale) {
+#define PHG_CASE(B, TT)                                                                 \
+    if (beta == B && T == TT) return ale ? fused_ptr<B, TT, true>() : fused_ptr<B, TT, false>();
+    PHG_CASE(1, 1) PHG_CASE(1, 2) PHG_CASE(1, 3) PHG_CASE(1, 4) PHG_CASE(1, 5) PHG_CASE(1, 6)
+    PHG_CASE(1, 7) PHG_CASE(1, 8) PHG_CASE(2, 1) PHG_CASE(2, 2) PHG_CASE(2, 3) PHG_CASE(2, 4)
+#undef PHG_CASE
+    return nullptr;
+}
+
+int max_fused(int beta) { return beta == 1 ? 5 : beta == 2 ? 4 : 0; }
+
+struct Launch {
+    int th;
+    int tiles_y;
+};
+
+// Output rows per tile: keep the staged region near 64 rows while not
+// wasting rows on a ragged last tile.
+Launch plan_rows(int own_rows, int halo) {
+    const int target = std::max(8, 64 - 2 * halo);
+    const int tiles = std::max(1, (own_rows + target - 1) / target);
+    const int th = (own_rows + tiles - 1) / tiles;
+    return {th, (own_rows + th - 1) / th};
+}
+
+int launch_fused(const phg_dev_image& src, const phg_dev_image& dst, int row_base, int height,
+                 int own_lo, int own_hi, const phg_params& p, int it0, int iters,
+                 uint64_t* counters, int kcap, cudaStream_t stream) {
+    FusedFn fn = select_fused(p.beta, iters, p.alpha <= 128);
+    if (!fn) return fail(PHG_EINVAL, "no fused kernel for this beta / iteration count");
+    const int halo = p.beta * iters;
+    const Launch L = plan_rows(own_hi - own_lo, halo);
+    const int sh = L.th + 2 * halo;
+    const size_t smem = 2ull * phg::buf_bytes(sh);
+    if (sh > 256) return fail(PHG_EINVAL, "tile too tall");
+    CUtensorMap map, apron;
+    PHG_TRY(encode_map(&map, src, phg::kHalfPx, sh));
+    PHG_TRY(encode_map(&apron, src, phg::kApronBox, sh));
+    PHG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    phg::TileArgs a;
+    a.dst = dst.data;
+    a.pitch = dst.pitch;
+    a.image_stride = dst.image_stride;
+    a.width = src.width;
+    a.height = height;
+    a.row_base = row_base;
+    a.own_lo = own_lo;
+    a.own_hi = own_hi;
+    a.th = L.th;
+    a.k7 = ((256u - static_cast<uint32_t>(p.alpha)) & 0x7fu) * 0x01010101u;
+    a.k_thr = (128u - static_cast<uint32_t>(std::min(p.card_threshold, 127))) * 0x01010101u;
+    a.alpha = p.alpha;
+    a.thr = p.card_threshold;
+    a.faithful = p.border == PHG_BORDER_FAITHFUL;
+    a.it0 = it0;
+    a.kcap = kcap;
+    a.counters = reinterpret_cast<unsigned long long*>(counters);
+    const int tiles_x = (src.width + phg::kOutPx - 1) / phg::kOutPx;
+    for (int z0 = 0; z0 < src.n_images; z0 += 65535) {
+        const int nz = std::min(65535, src.n_images - z0);
+        // images beyond the first chunk: offset the tensor map and pointers
+        CUtensorMap m2 = map, ap2 = apron;
+        phg::TileArgs a2 = a;
+        if (z0) {
+            phg_dev_image s2 = src;
+            s2.data += z0 * src.image_stride;
+            s2.n_images = nz;
+            PHG_TRY(encode_map(&m2, s2, phg::kHalfPx, sh));
+            PHG_TRY(encode_map(&ap2, s2, phg::kApronBox, sh));
+            a2.dst += z0 * dst.image_stride;
+            a2.counters += static_cast<int64_t>(z0) * kcap * 2;
+        }
+        dim3 grid(tiles_x, L.tiles_y, nz);
+        fn<<<grid, phg::kThreads, smem, stream>>>(m2, ap2, a2);
+        ++g_launches;
+        PHG_CUDA(cudaGetLastError());
+    }
+    return PHG_OK;
+}
+
+int launch_scalar(int mode, const phg_dev_image& src, const phg_dev_image* dst,
+                  const int32_t* card_in, int32_t* card_out, int64_t card_pitch, int row_base,
+                  int height, int own_lo, int own_hi, const phg_params& p, int it0,
+                  uint64_t* counters, int kcap, cudaStream_t stream) {
+    phg::ScalarArgs a;
+    a.src = src.data;
+    a.dst = dst ? dst->data : nullptr;
+    a.card_in = card_in;
+    a.card_out = card_out;
+    a.card_pitch = card_pitch;
+    a.pitch = src.pitch;
+    a.image_stride = src.image_stride;
+    a.width = src.width;
+    a.height = height;
+    a.row_base = row_base;
+    a.own_lo = own_lo;
+    a.own_hi = own_hi;
+    a.alpha = p.alpha;
+    a.beta = p.beta;
+    a.thr = p.card_threshold;
+    a.faithful = p.border == PHG_BORDER_FAITHFUL;
+    a.it0 = it0;
+    a.kcap = kcap;
+    a.counters = reinterpret_cast<unsigned long long*>(counters);
+    const int rows = own_hi - own_lo;
+    for (int z0 = 0; z0 < src.n_images; z0 += 65535) {
+        const int nz = std::min(65535, src.n_images - z0);
+        phg::ScalarArgs a2 = a;
+        a2.src += z0 * src.image_stride;
+        if (a2.dst) a2.dst += z0 * src.image_stride;
+        if (a2.counters) a2.counters += static_cast<int64_t>(z0) * kcap * 2;
+        if (a2.card_in) a2.card_in += static_cast<int64_t>(z0) * height * card_pitch;
+        if (a2.card_out) a2.card_out += static_cast<int64_t>(z0) * height * card_pitch;
+        for (int r0 = 0; r0 < rows; r0 += 65535) {
+            phg::ScalarArgs a3 = a2;
+            a3.own_lo = own_lo + r0;
+            a3.own_hi = std::min(own_hi, a3.own_lo + 65535);
+            dim3 grid((src.width + 255) / 256, a3.own_hi - a3.own_lo, nz);
+            if (mode == phg::kModeCard)
+                phg::scalar_kernel<phg::kModeCard><<<grid, 256, 0, stream>>>(a3);
+            else if (mode == phg::kModeRemoval)
+                phg::scalar_kernel<phg::kModeRemoval><<<grid, 256, 0, stream>>>(a3);
+            else
+                phg::scalar_kernel<phg::kModeFused><<<grid, 256, 0, stream>>>(a3);
+            ++g_launches;
+            PHG_CUDA(cudaGetLastError());
+        }
+    }
+    return PHG_OK;
+}
+
+// One chunk of `iters` iterations on a (band) buffer: fused TB kernel when
+// available, else one scalar fused launch per iteration (iters must be 1).
+int step(const phg_dev_image& src, const phg_dev_image& dst, int row_base, int height, int own_lo,
+         int own_hi, const phg_params& p, int it0, int iters, uint64_t* counters, int kcap,
+         cudaStream_t stream) {
+    if (max_fused(p.beta) > 0)
+        return launch_fused(src, dst, row_base, height, own_lo, own_hi, p, it0, iters, counters,
+                            kcap, stream);
+    if (iters != 1) return fail(PHG_EINVAL, "beta >= 3 runs one iteration per launch");
+    return launch_scalar(phg::kModeFused, src, &dst, nullptr, nullptr, 0, row_base, height, own_lo,
+                         own_hi, p, it0, counters, kcap, stream);
+}
+
+// Split k iterations into launches of at most max_fused(beta), evenly.
+std::vector<int> chunk_plan(int k, int beta) {
+    const int tmax = std::max(1, max_fused(beta));
+    const int n = (k + tmax - 1) / tmax;
+    std::vector<int> c(n, k / n);
+    for (int i = 0; i < k % n; ++i) ++c[i];
+    return c;
+}
+
+// ------------------------------------------------------- per-device state
+struct DeviceState {
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    std::vector<std::pair<void*, size_t>> bufs;  // grow-only scratch slots
+};
+
+std::mutex g_mu;
+std::vector<DeviceState> g_dev;
+
+int current_state(DeviceState** out, int* dev_out = nullptr) {
+    int dev = 0;
+    PHG_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (static_cast<int>(g_dev.size()) <= dev) g_dev.resize(dev + 1);
+    DeviceState& s = g_dev[dev];
+    if (!s.stream) {
+        PHG_CUDA(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+        PHG_CUDA(cudaEventCreate(&s.ev0));
+        PHG_CUDA(cudaEventCreate(&s.ev1));
+    }
+    *out = &s;
+    if (dev_out) *dev_out = dev;
+    return PHG_OK;
+}
+
+int scratch(DeviceState* s, int slot, size_t bytes, void** out) {
+    if (static_cast<int>(s->bufs.size()) <= slot) s->bufs.resize(slot + 1, {nullptr, 0});
+    auto& b = s->bufs[slot];
+    if (b.second < bytes) {
+        if (b.first) PHG_CUDA(cudaFree(b.first));
+        b.first = nullptr;
+        b.second = 0;
+        PHG_CUDA(cudaMalloc(&b.first, bytes));
+        b.second = bytes;
+    }
+    *out = b.first;
+    return PHG_OK;
+}
+
+phg_dev_image make_image(void* data, int w, int rows, int n) {
+    phg_dev_image im;
+    im.data = static_cast<uint8_t*>(data);
+    im.pitch = round_up(w, 16);
+    im.image_stride = im.pitch * rows;
+    im.width = w;
+    im.rows = rows;
+    im.n_images = n;
+    im._pad = 0;
+    return im;
+}
+
+int upload(const phg_dev_image& im, const uint8_t* host, cudaStream_t st) {
+    PHG_CUDA(cudaMemcpy2DAsync(im.data, im.pitch, host, im.width, im.width,
+                               static_cast<size_t>(im.rows) * im.n_images, cudaMemcpyHostToDevice, st));
+    return PHG_OK;
+}
+
+int download(uint8_t* host, const phg_dev_image& im, cudaStream_t st) {
+    PHG_CUDA(cudaMemcpy2DAsync(host, im.width, im.data, im.pitch, im.width,
+                               static_cast<size_t>(im.rows) * im.n_images, cudaMemcpyDeviceToHost, st));
+    return PHG_OK;
+}
+
+int finalize(const std::vector<uint64_t>& ctr, int n, int kcap, float ms, phg_pass_stats* stats,
+             int* iters) {
+    return phg_finalize_stats(ctr.data(), n, kcap, stats, iters) == PHG_OK
+               ? [&] {
+                     for (int i = 0; i < n; ++i) {
+                         const int it = iters[i];
+                         for (int j = 0; j < it; ++j)
+                             stats[static_cast<int64_t>(i) * kcap + j].elapsed_ms = ms / std::max(1, it);
+                     }
+                     return PHG_OK;
+                 }()
+               : PHG_EINVAL;
+}
+
+// ------------------------------------------------- band-sharded engine
+// The reference's Parallel engine splits rows with row_blocks
+// (denoise.hpp:97-107) and joins after every pass.  Here each band is a
+// separate device buffer holding its owned rows plus a beta*Tmax halo; after
+// every fused launch the halo rows are refreshed from the bands that own
+// them (the single-device stand-in for the NVLink / NCCL exchange of the
+// multi-GPU path in paper_1306_5390_b200/dist.py).
+struct Band {
+    int lo, hi;         // owned global rows
+    int blo, bhi;       // rows held in the buffer
+    phg_dev_image a, b; // ping-pong buffers
+};
+
+int denoise_bands(DeviceState* s, const phg_dev_image& in, int w, int h, const phg_params& p,
+                  int nbands, const phg_dev_image& out, uint64_t* counters) {
+    std::vector<Band> bands;
+    for (int k = 0; k < nbands; ++k) {
+        const int lo = static_cast<int>(static_cast<int64_t>(h) * k / nbands);
+        const int hi = static_cast<int>(static_cast<int64_t>(h) * (k + 1) / nbands);
+        if (hi > lo) bands.push_back({lo, hi, 0, 0, {}, {}});
+    }
+    const std::vector<int> plan = chunk_plan(p.max_iterations, p.beta);
+    const int tmax = *std::max_element(plan.begin(), plan.end());
+    const int halo = p.beta * tmax;
+    int slot = 8;
+    for (auto& b : bands) {
+        b.blo = std::max(0, b.lo - halo);
+        b.bhi = std::min(h, b.hi + halo);
+        void *pa, *pb;
+        const size_t bytes = static_cast<size_t>(round_up(w, 16)) * (b.bhi - b.blo);
+        PHG_TRY(scratch(s, slot++, bytes, &pa));
+        PHG_TRY(scratch(s, slot++, bytes, &pb));
+        b.a = make_image(pa, w, b.bhi - b.blo, 1);
+        b.b = make_image(pb, w, b.bhi - b.blo, 1);
+        // scatter the input (owned + halo rows) into the band's first buffer
+        PHG_CUDA(cudaMemcpy2DAsync(b.a.data, b.a.pitch, in.data + static_cast<int64_t>(b.blo) * in.pitch,
+                                   in.pitch, w, b.bhi - b.blo, cudaMemcpyDeviceToDevice, s->stream));
+    }
+    int it0 = 0;
+    for (size_t c = 0; c < plan.size(); ++c) {
+        for (auto& b : bands)
+            PHG_TRY(step(b.a, b.b, b.blo, h, b.lo, b.hi, p, it0, plan[c], counters,
+                         p.max_iterations, s->stream));
+        // halo exchange: every halo row of band i comes from its owner band
+        for (auto& b : bands) {
+            for (auto& o : bands) {
+                if (&o == &b) continue;
+                const int r0 = std::max(b.blo, o.lo), r1 = std::min(b.bhi, o.hi);
+                if (r1 <= r0) continue;
+                PHG_CUDA(cudaMemcpy2DAsync(b.b.data + static_cast<int64_t>(r0 - b.blo) * b.b.pitch,
+                                           b.b.pitch,
+                                           o.b.data + static_cast<int64_t>(r0 - o.blo) * o.b.pitch,
+                                           o.b.pitch, w, r1 - r0, cudaMemcpyDeviceToDevice, s->stream));
+            }
+        }
+        for (auto& b : bands) std::swap(b.a, b.b);
+        it0 += plan[c];
+    }
+    for (auto& b : bands)
+        PHG_CUDA(cudaMemcpy2DAsync(out.data + static_cast<int64_t>(b.lo) * out.pitch, out.pitch,
+                                   b.a.data + static_cast<int64_t>(b.lo - b.blo) * b.a.pitch, b.a.pitch, w,
+                                   b.hi - b.lo, cudaMemcpyDeviceToDevice, s->stream));
+    return PHG_OK;
+}
+
+// -------------------------------------------- host generators (restated)
+// synth_image (image.hpp:53-106): std::mt19937's sequence is fixed by the
+// C++ standard, so this reproduces the reference bit for bit.
+void synth(int w, int h, uint32_t seed, int kind, uint8_t* out) {
+    const size_t n = static_cast<size_t>(w) * h;
+    if (kind == 0) {
+        for (int r = 0; r < h; ++r)
+            for (int c = 0; c < w; ++c)
+                out[static_cast<size_t>(r) * w + c] =
+                    static_cast<uint8_t>(w == 1 ? 0 : static_cast<int>(255LL * c / (w - 1)));
+        return;
+    }
+    if (kind == 1) {
+        for (int r = 0; r < h; ++r)
+            for (int c = 0; c < w; ++c) out[static_cast<size_t>(r) * w + c] = ((r / 8 + c / 8) & 1) ? 192 : 64;
+        return;
+    }
+    std::mt19937 gen(seed);
+    std::vector<uint8_t> raw(n);
+    for (auto& v : raw) v = static_cast<uint8_t>(gen() & 0xffu);
+    for (int r = 0; r < h; ++r) {
+        const int ra = std::max(0, r - 1), rb = std::min(h - 1, r + 1);
+        for (int c = 0; c < w; ++c) {
+            const int ca = std::max(0, c - 1), cb = std::min(w - 1, c + 1);
+            int sum = 0;
+            const int cnt = (rb - ra + 1) * (cb - ca + 1);
+            for (int i = ra; i <= rb; ++i)
+                for (int j = ca; j <= cb; ++j) sum += raw[static_cast<size_t>(i) * w + j];
+            out[static_cast<size_t>(r) * w + c] = static_cast<uint8_t>(std::min(255, (sum + cnt / 2) / cnt));
+        }
+    }
+}
+
+}  // namespace
+
+// ====================================================================== ABI
+extern "C" {
+
+int phg_abi_version(void) { return PHG_ABI_VERSION; }
+const char* phg_last_error(void) { return g_error.c_str(); }
+int phg_validate_params(const phg_params* p) { return validate(p); }
+int64_t phg_launch_count(void) { return g_launches; }
+void phg_reset_launch_count(void) { g_launches = 0; }
+
+int phg_device_count(int* count) {
+    PHG_CUDA(cudaGetDeviceCount(count));
+    return PHG_OK;
+}
+
+int phg_set_device(int device) {
+    PHG_CUDA(cudaSetDevice(device));
+    return PHG_OK;
+}
+
+int phg_max_fused_iterations(int beta) { return max_fused(beta); }
+
+int phg_finalize_stats(const uint64_t* ctr, int n, int kcap, phg_pass_stats* stats, int* iterations_run) {
+    if (!ctr || !stats || !iterations_run || n < 0 || kcap < 1) return fail(PHG_EINVAL, "bad arguments");
+    for (int i = 0; i < n; ++i) {
+        int it = 0;
+        for (int j = 0; j < kcap; ++j) {
+            phg_pass_stats& s = stats[static_cast<int64_t>(i) * kcap + j];
+            s.iteration = j + 1;
+            s._pad = 0;
+            s.flagged = static_cast<int64_t>(ctr[(static_cast<int64_t>(i) * kcap + j) * 2]);
+            s.replaced = static_cast<int64_t>(ctr[(static_cast<int64_t>(i) * kcap + j) * 2 + 1]);
+            s.elapsed_ms = 0.0;
+            it = j + 1;
+            if (s.replaced == 0) break;  // denoise.hpp:308
+        }
+        iterations_run[i] = it;
+    }
+    return PHG_OK;
+}
+
+int phg_dev_fused_step(const phg_dev_image* src, const phg_dev_image* dst, int row_base, int height,
+                       int own_lo, int own_hi, const phg_params* p, int it0, int iters,
+                       uint64_t* counters, int kcap, void* stream) {
+    PHG_TRY(validate(p));
+    if (!src || !dst || own_lo < 0 || own_hi > height || own_lo >= own_hi || iters < 1 ||
+        it0 < 0 || it0 + iters > kcap)
+        return fail(PHG_EINVAL, "bad band geometry");
+    if (max_fused(p->beta) > 0 && iters > max_fused(p->beta))
+        return fail(PHG_EINVAL, "iters exceeds phg_max_fused_iterations(beta)");
+    return step(*src, *dst, row_base, height, own_lo, own_hi, *p, it0, iters, counters, kcap,
+                static_cast<cudaStream_t>(stream));
+}
+
+int phg_dev_denoise(const phg_dev_image* src, const phg_dev_image* dst, const phg_dev_image* tmp,
+                    const phg_params* p, uint64_t* counters, void* stream) {
+    PHG_TRY(validate(p));
+    if (!src || !dst || !tmp) return fail(PHG_EINVAL, "null image");
+    PHG_TRY(check_dims(src->width, src->rows));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int k = p->max_iterations;
+    PHG_CUDA(cudaMemsetAsync(counters, 0, sizeof(uint64_t) * 2 * k * src->n_images, st));
+    const std::vector<int> plan = max_fused(p->beta) > 0 ? chunk_plan(k, p->beta) : std::vector<int>(k, 1);
+    const int nl = static_cast<int>(plan.size());
+    const phg_dev_image* cur = src;
+    int it0 = 0;
+    for (int i = 0; i < nl; ++i) {
+        const phg_dev_image* out = ((nl - 1 - i) % 2 == 0) ? dst : tmp;
+        PHG_TRY(step(*cur, *out, 0, src->rows, 0, src->rows, *p, it0, plan[i], counters, k, st));
+        cur = out;
+        it0 += plan[i];
+    }
+    return PHG_OK;
+}
+
+int phg_dev_cardinality(const phg_dev_image* src, int alpha, int beta, int32_t* card, int64_t card_pitch,
+                        void* stream) {
+    phg_params p{alpha, beta, 1, 1, 0};
+    if (alpha < 1 || alpha > 255) return fail(PHG_EINVAL, "alpha must be in [1, 255]");
+    if (beta < 1) return fail(PHG_EINVAL, "beta must be >= 1");
+    return launch_scalar(phg::kModeCard, *src, nullptr, nullptr, card, card_pitch, 0, src->rows, 0,
+                         src->rows, p, 0, nullptr, 1, static_cast<cudaStream_t>(stream));
+}
+
+int phg_dev_removal(const phg_dev_image* src, const int32_t* card, int64_t card_pitch, const phg_params* p,
+                    const phg_dev_image* dst, uint64_t* counters, void* stream) {
+    PHG_TRY(validate(p));
+    return launch_scalar(phg::kModeRemoval, *src, dst, card, nullptr, card_pitch, 0, src->rows, 0,
+                         src->rows, *p, 0, counters, 1, static_cast<cudaStream_t>(stream));
+}
+
+int phg_cardinality(const uint8_t* img, int w, int h, int alpha, int beta, int32_t* counts) {
+    if (alpha < 1 || alpha > 255) return fail(PHG_EINVAL, "alpha must be in [1, 255]");
+    if (beta < 1) return fail(PHG_EINVAL, "beta must be >= 1");
+    PHG_TRY(check_dims(w, h));
+    DeviceState* s;
+    PHG_TRY(current_state(&s));
+    void *pi, *pc;
+    const phg_dev_image in = make_image(nullptr, w, h, 1);
+    const int64_t cpitch = round_up(w, 4);
+    PHG_TRY(scratch(s, 0, in.image_stride, &pi));
+    PHG_TRY(scratch(s, 3, sizeof(int32_t) * cpitch * h, &pc));
+    phg_dev_image im = make_image(pi, w, h, 1);
+    PHG_TRY(upload(im, img, s->stream));
+    PHG_TRY(phg_dev_cardinality(&im, alpha, beta, static_cast<int32_t*>(pc), cpitch, s->stream));
+    PHG_CUDA(cudaMemcpy2DAsync(counts, sizeof(int32_t) * w, pc, sizeof(int32_t) * cpitch,
+                               sizeof(int32_t) * w, h, cudaMemcpyDeviceToHost, s->stream));
+    PHG_CUDA(cudaStreamSynchronize(s->stream));
+    return PHG_OK;
+}
+
+int phg_denoise_pass(const uint8_t* img, int w, int h, const int32_t* card, int cw, int ch,
+                     const phg_params* p, uint8_t* out, phg_pass_stats* stats) {
+    PHG_TRY(validate(p));
+    if (cw != w || ch != h) return fail(PHG_EINVAL, "cardinality map does not match image");
+    PHG_TRY(check_dims(w, h));
+    DeviceState* s;
+    PHG_TRY(current_state(&s));
+    void *pi, *po, *pc, *pk;
+    const int64_t cpitch = round_up(w, 4);
+    const phg_dev_image probe = make_image(nullptr, w, h, 1);
+    PHG_TRY(scratch(s, 0, probe.image_stride, &pi));
+    PHG_TRY(scratch(s, 1, probe.image_stride, &po));
+    PHG_TRY(scratch(s, 3, sizeof(int32_t) * cpitch * h, &pc));
+    PHG_TRY(scratch(s, 4, sizeof(uint64_t) * 2, &pk));
+    phg_dev_image im = make_image(pi, w, h, 1), om = make_image(po, w, h, 1);
+    PHG_TRY(upload(im, img, s->stream));
+    PHG_CUDA(cudaMemcpy2DAsync(pc, sizeof(int32_t) * cpitch, card, sizeof(int32_t) * w, sizeof(int32_t) * w, h,
+                               cudaMemcpyHostToDevice, s->stream));
+    PHG_CUDA(cudaMemsetAsync(pk, 0, sizeof(uint64_t) * 2, s->stream));
+    PHG_CUDA(cudaEventRecord(s->ev0, s->stream));
+    PHG_TRY(phg_dev_removal(&im, static_cast<int32_t*>(pc), cpitch, p, &om, static_cast<uint64_t*>(pk),
+                            s->stream));
+    PHG_CUDA(cudaEventRecord(s->ev1, s->stream));
+    PHG_TRY(download(out, om, s->stream));
+    uint64_t ctr[2];
+    PHG_CUDA(cudaMemcpyAsync(ctr, pk, sizeof(ctr), cudaMemcpyDeviceToHost, s->stream));
+    PHG_CUDA(cudaStreamSynchronize(s->stream));
+    float ms = 0;
+    PHG_CUDA(cudaEventElapsedTime(&ms, s->ev0, s->ev1));
+    stats->iteration = 1;
+    stats->_pad = 0;
+    stats->flagged = static_cast<int64_t>(ctr[0]);
+    stats->replaced = static_cast<int64_t>(ctr[1]);
+    stats->elapsed_ms = ms;
+    return PHG_OK;
+}
+
+int phg_denoise(const uint8_t* img, int w, int h, const phg_params* p, int bands, uint8_t* out,
+                phg_pass_stats* stats, int* iterations_run) {
+    PHG_TRY(validate(p));
+    PHG_TRY(check_dims(w, h));
+    DeviceState* s;
+    PHG_TRY(current_state(&s));
+    const int k = p->max_iterations;
+    void *pi, *pa, *pb, *pk;
+    const phg_dev_image probe = make_image(nullptr, w, h, 1);
+    PHG_TRY(scratch(s, 0, probe.image_stride, &pi));
+    PHG_TRY(scratch(s, 1, probe.image_stride, &pa));
+    PHG_TRY(scratch(s, 2, probe.image_stride, &pb));
+    PHG_TRY(scratch(s, 4, sizeof(uint64_t) * 2 * k, &pk));
+    phg_dev_image im = make_image(pi, w, h, 1), am = make_image(pa, w, h, 1), bm = make_image(pb, w, h, 1);
+    uint64_t* ctr = static_cast<uint64_t*>(pk);
+    PHG_TRY(upload(im, img, s->stream));
+    PHG_CUDA(cudaEventRecord(s->ev0, s->stream));
+    if (bands <= 1) {
+        PHG_TRY(phg_dev_denoise(&im, &am, &bm, p, ctr, s->stream));
+    } else {
+        PHG_CUDA(cudaMemsetAsync(ctr, 0, sizeof(uint64_t) * 2 * k, s->stream));
+        PHG_TRY(denoise_bands(s, im, w, h, *p, bands, am, ctr));
+    }
+    PHG_CUDA(cudaEventRecord(s->ev1, s->stream));
+    PHG_TRY(download(out, am, s->stream));
+    std::vector<uint64_t> hc(2 * k);
+    PHG_CUDA(cudaMemcpyAsync(hc.data(), ctr, sizeof(uint64_t) * 2 * k, cudaMemcpyDeviceToHost, s->stream));
+    PHG_CUDA(cudaStreamSynchronize(s->stream));
+    float ms = 0;
+    PHG_CUDA(cudaEventElapsedTime(&ms, s->ev0, s->ev1));
+    return finalize(hc, 1, k, ms, stats, iterations_run);
+}
+
+int phg_denoise_batch(const uint8_t* imgs, int n, int w, int h, const phg_params* p, uint8_t* out,
+                      phg_pass_stats* stats, int* iterations_run) {
+    PHG_TRY(validate(p));
+    PHG_TRY(check_dims(w, h));
+    if (n < 1) return fail(PHG_EINVAL, "batch must hold at least one image");
+    DeviceState* s;
+    PHG_TRY(current_state(&s));
+    const int k = p->max_iterations;
+    void *pi, *pa, *pb, *pk;
+    const phg_dev_image probe = make_image(nullptr, w, h, n);
+    const size_t bytes = static_cast<size_t>(probe.image_stride) * n;
+    PHG_TRY(scratch(s, 0, bytes, &pi));
+    PHG_TRY(scratch(s, 1, bytes, &pa));
+    PHG_TRY(scratch(s, 2, bytes, &pb));
+    PHG_TRY(scratch(s, 4, sizeof(uint64_t) * 2 * k * n, &pk));
+    phg_dev_image im = make_image(pi, w, h, n), am = make_image(pa, w, h, n), bm = make_image(pb, w, h, n);
+    uint64_t* ctr = static_cast<uint64_t*>(pk);
+    PHG_TRY(upload(im, imgs, s->stream));
+    PHG_CUDA(cudaEventRecord(s->ev0, s->stream));
+    PHG_TRY(phg_dev_denoise(&im, &am, &bm, p, ctr, s->stream));
+    PHG_CUDA(cudaEventRecord(s->ev1, s->stream));
+    PHG_TRY(download(out, am, s->stream));
+    std::vector<uint64_t> hc(static_cast<size_t>(2) * k * n);
+    PHG_CUDA(cudaMemcpyAsync(hc.data(), ctr, sizeof(uint64_t) * hc.size(), cudaMemcpyDeviceToHost, s->stream));
+    PHG_CUDA(cudaStreamSynchronize(s->stream));
+    float ms = 0;
+    PHG_CUDA(cudaEventElapsedTime(&ms, s->ev0, s->ev1));
+    return finalize(hc, n, k, ms / n, stats, iterations_run);
+}
+
+int phg_synth_image(int w, int h, uint32_t seed, int kind, uint8_t* out) {
+    PHG_TRY(check_dims(w, h));
+    if (kind < 0 || kind > 2) return fail(PHG_EINVAL, "unknown synth kind");
+    synth(w, h, seed, kind, out);
+    return PHG_OK;
+}
+
+// inject_sp_noise (noise.hpp:62-89): exact-count salt & pepper, partial
+// Fisher-Yates over uint32 indices driven by mt19937 with rejection draws.
+int64_t phg_inject_sp_noise(const uint8_t* img, int w, int h, double density, double salt_ratio,
+                            uint32_t seed, uint8_t* out, uint8_t* mask) {
+    if (!(density >= 0.0 && density <= 1.0)) return fail(PHG_EINVAL, "density must be in [0, 1]");
+    if (!(salt_ratio >= 0.0 && salt_ratio <= 1.0)) return fail(PHG_EINVAL, "salt_ratio must be in [0, 1]");
+    PHG_TRY(check_dims(w, h));
+    const uint64_t total = static_cast<uint64_t>(w) * h;
+    if (total > 0xffffffffull) return fail(PHG_EINVAL, "inject_sp_noise: image exceeds 2^32 - 1 pixels");
+    const uint64_t n = static_cast<uint64_t>(std::llround(density * static_cast<double>(total)));
+    const uint64_t salt = static_cast<uint64_t>(std::llround(salt_ratio * static_cast<double>(n)));
+    std::memcpy(out, img, total);
+    if (mask) std::memset(mask, 0, total);
+    if (n == 0) return 0;
+    std::vector<uint32_t> idx(total);
+    std::iota(idx.begin(), idx.end(), 0u);
+    std::mt19937 gen(seed);
+    for (uint64_t i = 0; i < n; ++i) {
+        const uint32_t bound = static_cast<uint32_t>(total - i);
+        const uint32_t reject_below = (0u - bound) % bound;
+        uint32_t r;
+        do r = gen(); while (r < reject_below);
+        const uint64_t j = i + r % bound;
+        std::swap(idx[i], idx[j]);
+        out[idx[i]] = i < salt ? 255 : 0;
+        if (mask) mask[idx[i]] = 1;
+    }
+    return static_cast<int64_t>(n);
+}
+
+}  // extern "C"
