@@ -20,27 +20,36 @@
 namespace phg {
 
 // ------------------------------------------------------------ geometry
-// A tile stages region columns [x0, x0+528) with x0 = tile*496 - 16: a
-// 16-px left apron (TMA tile boxes need a 16-byte aligned innermost start
-// coordinate, so the apron cannot be narrower), 496 output px and a 16-px
-// right apron.  Three TMA boxes fill one shared buffer laid out as
-// [SH][256] | [SH][256] | [SH][16].  The 128 threads of a row group compute
-// region words 2..129 (8 px either side of the output, so beta*T <= 8).
+// A tile stages region columns [x0, x0+528) with x0 = tile*496 - 16 into one
+// dense shared buffer [SH][528]: a 16-px left apron (TMA tile boxes need a
+// 16-byte aligned innermost start coordinate, so the apron cannot be
+// narrower), 496 output px and a 16-px right apron.  The image is viewed by
+// the tensor map as [images][rows][chunks][16 px], so ONE 4-D box
+// {16, 33, SH, 1} lands as the dense [SH][528] tile.  The 128 threads of a
+// row group compute region words 2..129 (8 px either side of the output,
+// so beta*T <= 8).
 constexpr int kLeftPx = 16;
 constexpr int kOutPx = 496;
-constexpr int kRegionPx = kLeftPx + kOutPx + 16;  // 528
-constexpr int kCompWords = 128;                  // words 2..129
+constexpr int kRP = kLeftPx + kOutPx + 16;  // 528 = shared row pitch
+constexpr int kChunk = 16;
+constexpr int kChunks = kRP / kChunk;       // 33
+constexpr int kCompWords = 128;             // region words 2..129
 constexpr int kFirstWord = 2;
-constexpr int kOutWordLo = kLeftPx / 4;          // 4
+constexpr int kOutWordLo = kLeftPx / 4;     // 4
 constexpr int kOutWordHi = kOutWordLo + kOutPx / 4;  // 128
-constexpr int kGroups = 2;                       // row groups per CTA
+constexpr int kGroups = 2;                  // row groups per CTA
 constexpr int kThreads = kCompWords * kGroups;
-constexpr int kHalfPx = 256;                     // wide TMA box
-constexpr int kApronBox = 16;                    // narrow TMA box
+constexpr int kWarps = kThreads / 32;
 constexpr int kMaxHaloPx = 8;
+constexpr int kListCap = kCompWords * 4;    // per-warp candidate list (one row)
 
 // bytes of one staged buffer of sh rows (rounded for 128-B alignment)
-__host__ __device__ constexpr int buf_bytes(int sh) { return (kRegionPx * sh + 127) / 128 * 128; }
+__host__ __device__ constexpr int buf_bytes(int sh) { return (kRP * sh + 127) / 128 * 128; }
+// two staged buffers + candidate bitmap (one nibble-byte per word and row)
+// + per-warp candidate lists
+__host__ __device__ constexpr int smem_bytes(int sh) {
+    return 2 * buf_bytes(sh) + (kCompWords * sh + 127) / 128 * 128 + kWarps * kListCap * 2;
+}
 
 struct TileArgs {
     uint8_t* dst;
@@ -87,41 +96,26 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
         : "memory");
 }
 
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z,
-                                            uint64_t* bar) {
+// 4-D tile load: coordinates {px-in-chunk, chunk, row, image}.
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            int c3, uint64_t* bar) {
     asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
         : "memory");
 }
 
-// Shared-memory location of region word w: byte offset at row 0 and the
-// row pitch of the segment it lives in.
-struct WordLoc {
-    int off;
-    int pitch;
-};
+__device__ __forceinline__ uint32_t lds32(const uint8_t* p) { return *reinterpret_cast<const uint32_t*>(p); }
 
-__device__ __forceinline__ WordLoc word_loc(int w, int sh) {
-    const int px = 4 * w;
-    if (px < kHalfPx) return {px, kHalfPx};
-    if (px < 2 * kHalfPx) return {kHalfPx * sh + px - kHalfPx, kHalfPx};
-    return {2 * kHalfPx * sh + px - 2 * kHalfPx, kApronBox};
-}
-
-__device__ __forceinline__ uint32_t lds_word(const uint8_t* buf, WordLoc l, int y) {
-    return *reinterpret_cast<const uint32_t*>(buf + l.off + y * l.pitch);
-}
-
-// Loads the 2*BETA+1 column-shifted variants of region row y around the
-// thread's word: v[BETA+dc] holds, in byte j, the pixel at column 4w+j+dc.
+// Loads the 2*BETA+1 column-shifted variants of a staged row around the
+// thread's word (rowp points at the word): v[BETA+dc] holds, in byte j, the
+// pixel at column 4w+j+dc.
 template <int BETA>
-__device__ __forceinline__ void load_row(const uint8_t* buf, WordLoc ll, WordLoc lc, WordLoc lr,
-                                         int y, uint32_t (&v)[2 * BETA + 1]) {
-    const uint32_t c = lds_word(buf, lc, y);
-    const uint32_t l = lds_word(buf, ll, y);
-    const uint32_t r = lds_word(buf, lr, y);
+__device__ __forceinline__ void load_row(const uint8_t* rowp, uint32_t (&v)[2 * BETA + 1]) {
+    const uint32_t c = lds32(rowp);
+    const uint32_t l = lds32(rowp - 4);
+    const uint32_t r = lds32(rowp + 4);
 #pragma unroll
     for (int dc = 1; dc <= BETA; ++dc) {
         v[BETA - dc] = __funnelshift_l(l, c, 8 * dc);
@@ -150,43 +144,67 @@ __device__ __forceinline__ uint32_t count_similar(const uint32_t (&win)[2 * BETA
     return cnt;
 }
 
-// Decides one flagged lane exactly as removal_rows (denoise.hpp:192-217)
-// and returns the replacement value, or -1 when the pixel is kept.
+// round(sqrt(S/f)) half away from zero, exact for S <= 2^24 / 4, f <= 2^10:
+// r ~ sqrt(4S/f) (few-ulp estimate); the answer floor((sqrt(4S/f)+1)/2)
+// only changes at odd r, so m = nearest(r) decides it except when m is odd,
+// where m^2 f <= 4S settles the tie exactly in integers.
+__device__ __forceinline__ uint32_t rms_round32(uint32_t S, uint32_t f) {
+    const float x = fmaxf(__fdividef(static_cast<float>(4u * S), static_cast<float>(f)), 1e-30f);
+    const float r = x * rsqrtf(x);
+    const int m = __float2int_rn(r);
+    if (m & 1) return (static_cast<uint32_t>(m * m) * f <= 4u * S) ? (m + 1) >> 1 : (m - 1) >> 1;
+    return static_cast<uint32_t>(m) >> 1;
+}
+
+// One candidate pixel: decide and compute the RMS replacement exactly as
+// removal_rows (denoise.hpp:192-217).  Returns 1 if it is an owned pixel
+// that was replaced (for the per-iteration counters).
 template <int BETA>
-__device__ __forceinline__ int lane_replacement(const uint32_t (&win)[2 * BETA + 1][2 * BETA + 1],
-                                                const uint32_t (&colm)[2 * BETA + 1],
-                                                const uint32_t (&rowm)[2 * BETA + 1], int lane,
-                                                int alpha, int faithful) {
-    const int sh = 8 * lane;
-    const int p = (win[BETA][BETA] >> sh) & 0xff;
-    uint32_t S = 0;
-    int flag = 0, inb = 0;
+__device__ __forceinline__ uint32_t process_pixel(int y, int px, const uint8_t* src, uint8_t* dst,
+                                                  int gx0, int gy0, int own_y_lo, int own_y_hi,
+                                                  const TileArgs& a) {
+    const uint8_t* c = src + y * kRP + px;
+    const int p = *c;
+    const int gr = gy0 + y, gc = gx0 + px;
+    uint32_t S = 0, f = 0;
+    int pix_count;
+    if (gr >= BETA && gr < a.height - BETA && gc >= BETA && gc < a.width - BETA) {
 #pragma unroll
-    for (int i = 0; i < 2 * BETA + 1; ++i) {
+        for (int dy = -BETA; dy <= BETA; ++dy)
 #pragma unroll
-        for (int j = 0; j < 2 * BETA + 1; ++j) {
-            const bool ok = ((colm[j] & rowm[i]) >> (sh + 7)) & 1u;
-            if (i == BETA && j == BETA) {
-                ++inb;
-                continue;
+            for (int dx = -BETA; dx <= BETA; ++dx) {
+                if (dy == 0 && dx == 0) continue;
+                const int q = c[dy * kRP + dx];
+                const bool dis = abs(q - p) >= a.alpha;
+                S += dis ? static_cast<uint32_t>(q * q) : 0u;
+                f += dis;
             }
-            const int q = (win[i][j] >> sh) & 0xff;
-            const bool dis = ok && abs(q - p) >= alpha;
-            inb += ok;
-            flag += dis;
-            S += dis ? static_cast<uint32_t>(q * q) : 0u;
-        }
+        pix_count = (2 * BETA + 1) * (2 * BETA + 1);
+    } else {
+        int inb = 0;
+        for (int dy = -BETA; dy <= BETA; ++dy)
+            for (int dx = -BETA; dx <= BETA; ++dx) {
+                const int rr = gr + dy, cc = gc + dx;
+                if (rr < 0 || rr >= a.height || cc < 0 || cc >= a.width) continue;
+                ++inb;
+                const int q = c[dy * kRP + dx];
+                const bool dis = abs(q - p) >= a.alpha;
+                S += dis ? static_cast<uint32_t>(q * q) : 0u;
+                f += dis;
+            }
+        pix_count = a.faithful ? (2 * BETA + 1) * (2 * BETA + 1) : inb;
     }
-    const int window = (2 * BETA + 1) * (2 * BETA + 1);
-    const int pix_count = faithful ? window : inb;
-    if (flag > pix_count - 3 && flag > 0) return static_cast<int>(rms_round(S, flag));
-    return -1;
+    if (static_cast<int>(f) > pix_count - 3 && f > 0) {
+        dst[y * kRP + px] = static_cast<uint8_t>(rms_round32(S, f));
+        return (y >= own_y_lo && y < own_y_hi && px >= kLeftPx && px < kLeftPx + kOutPx && gc < a.width) ? 1u
+                                                                                                         : 0u;
+    }
+    return 0;
 }
 
 template <int BETA, int T, bool ALE>
 __global__ void __launch_bounds__(kThreads)
-    fused_tb_kernel(const __grid_constant__ CUtensorMap src_map,
-                    const __grid_constant__ CUtensorMap apron_map, const TileArgs a) {
+    fused_tb_kernel(const __grid_constant__ CUtensorMap src_map, const TileArgs a) {
     static_assert(BETA * T <= kMaxHaloPx, "halo exceeds the staged columns");
     constexpr int HALO = BETA * T;
     constexpr int NB = 2 * BETA + 1;
@@ -196,26 +214,28 @@ __global__ void __launch_bounds__(kThreads)
 
     const int sh = a.th + 2 * HALO;
     uint8_t* buf[2] = {smem, smem + buf_bytes(sh)};
+    const int lane = threadIdx.x & 31;
+    uint8_t* cmap = smem + 2 * buf_bytes(sh);  // [sh][128] candidate nibbles
+    uint16_t* list = reinterpret_cast<uint16_t*>(cmap + (kCompWords * sh + 127) / 128 * 128) +
+                     (threadIdx.x >> 5) * kListCap;
 
     const int img = blockIdx.z;
-    const int x0 = blockIdx.x * kOutPx - kLeftPx;  // global col of region col 0 (16-aligned)
+    const int x0 = blockIdx.x * kOutPx - kLeftPx;  // global col of region px 0 (16-aligned)
     const int out_r0 = (a.own_lo - a.row_base) + blockIdx.y * a.th;  // buffer row
     const int out_rows = min(a.th, (a.own_hi - a.row_base) - out_r0);
     const int y0 = out_r0 - HALO;  // buffer row of region row 0
+    const int gy0 = a.row_base + y0;  // global row of region row 0
 
     if (threadIdx.x == 0) {
         mbar_init(&bar, 1);
-        mbar_expect_tx(&bar, static_cast<uint32_t>(kRegionPx * sh));
-        tma_load_3d(buf[0], &src_map, x0, y0, img, &bar);
-        tma_load_3d(buf[0] + kHalfPx * sh, &src_map, x0 + kHalfPx, y0, img, &bar);
-        tma_load_3d(buf[0] + 2 * kHalfPx * sh, &apron_map, x0 + 2 * kHalfPx, y0, img, &bar);
+        mbar_expect_tx(&bar, static_cast<uint32_t>(kRP * sh));
+        tma_load_4d(buf[0], &src_map, 0, x0 / kChunk, y0, img, &bar);
     }
     if (threadIdx.x < 2 * T) red[threadIdx.x >> 1][threadIdx.x & 1] = 0;
 
     const int w = kFirstWord + threadIdx.x % kCompWords;  // region word
     const int g = threadIdx.x / kCompWords;
     const int gcol = x0 + 4 * w;  // global col of lane 0
-    const WordLoc lc = word_loc(w, sh), ll = word_loc(w - 1, sh), lr = word_loc(w + 1, sh);
 
     uint32_t colm[NB];
 #pragma unroll
@@ -250,72 +270,91 @@ __global__ void __launch_bounds__(kThreads)
         const int ylo = max(g_lo, BETA * (t + 1));
         const int yhi = min(g_hi, sh - BETA * (t + 1));
         uint32_t win[NB][NB];
+        const uint8_t* colp = src + 4 * w;
         if (ylo < yhi) {
 #pragma unroll
-            for (int i = 0; i < NB - 1; ++i) load_row<BETA>(src, ll, lc, lr, ylo - BETA + i, win[i]);
+            for (int i = 0; i < NB - 1; ++i) load_row<BETA>(colp + (ylo - BETA + i) * kRP, win[i]);
         }
         for (int y = ylo; y < yhi; ++y) {
-            load_row<BETA>(src, ll, lc, lr, y + BETA, win[NB - 1]);
-            const int gr = a.row_base + y0 + y;  // global row
+            load_row<BETA>(colp + (y + BETA) * kRP, win[NB - 1]);
+            const int gr = gy0 + y;  // global row
             const bool rows_ok = (gr - BETA >= 0) && (gr + BETA < a.height);
-            const bool row_in = (gr >= 0) && (gr < a.height);
-            uint32_t rowm[NB];
+            uint32_t cnt;
+            if (rows_ok) {
+                uint32_t rowm[NB];
 #pragma unroll
-            for (int i = 0; i < NB; ++i) {
-                const int rr = gr + i - BETA;
-                rowm[i] = (rr >= 0 && rr < a.height) ? 0xffffffffu : 0u;
+                for (int i = 0; i < NB; ++i) rowm[i] = 0xffffffffu;
+                cnt = count_similar<BETA, ALE, true>(win, colm, rowm, a.k7);
+            } else {
+                uint32_t rowm[NB];
+#pragma unroll
+                for (int i = 0; i < NB; ++i) {
+                    const int rr = gr + i - BETA;
+                    rowm[i] = (rr >= 0 && rr < a.height) ? 0xffffffffu : 0u;
+                }
+                cnt = count_similar<BETA, ALE, false>(win, colm, rowm, a.k7);
             }
-            const uint32_t cnt = rows_ok ? count_similar<BETA, ALE, true>(win, colm, rowm, a.k7)
-                                         : count_similar<BETA, ALE, false>(win, colm, rowm, a.k7);
             const uint32_t card = cnt + 0x01010101u;
+            const bool row_in = (gr >= 0) && (gr < a.height);
             const uint32_t inimg = row_in ? inimg_col : 0u;
             const uint32_t flagged = lt_bits(card, a.k_thr) & inimg;
-            uint32_t out = win[BETA][BETA];
-            uint32_t rep = 0;
-            if (flagged) {
-                if (rows_ok && !col_border) {
-                    // interior: in_bounds = pix_count = (2B+1)^2, so
-                    // flag > pix_count-3 <=> card < 3 (and flag > 0 holds).
-                    rep = flagged & lt_bits(card, rep4(125u));
-                    uint32_t m = rep;
-                    while (m) {
-                        const int lane = (__ffs(m) - 8) >> 3;
-                        m &= m - 1;
-                        const int v = lane_replacement<BETA>(win, colm, rowm, lane, a.alpha, a.faithful);
-                        out = (out & ~(0xffu << (8 * lane))) | (static_cast<uint32_t>(v) << (8 * lane));
-                    }
-                } else {
-                    uint32_t m = flagged;
-                    while (m) {
-                        const int lane = (__ffs(m) - 8) >> 3;
-                        m &= m - 1;
-                        const int v = lane_replacement<BETA>(win, colm, rowm, lane, a.alpha, a.faithful);
-                        if (v >= 0) {
-                            rep |= 0x80u << (8 * lane);
-                            out = (out & ~(0xffu << (8 * lane))) | (static_cast<uint32_t>(v) << (8 * lane));
-                        }
-                    }
-                }
-            }
-            const bool own_row = (y >= HALO) && (y < HALO + out_rows);
-            if (own_row) {
-                nfl[t] += __popc(flagged & own_col);
-                nrp[t] += __popc(rep & own_col);
-            }
-            if (t == T - 1) {
-                if (own_row && own_word && gcol < a.width) {
-                    uint8_t* p = a.dst + img * a.image_stride + (int64_t)(y0 + y) * a.pitch + gcol;
-                    *reinterpret_cast<uint32_t*>(p) = out;
-                }
-            } else {
-                *reinterpret_cast<uint32_t*>(dstb + lc.off + y * lc.pitch) = out;
-            }
+            // interior: in_bounds = pix_count = (2B+1)^2, so
+            // flag > pix_count-3 <=> card < 3 (and flag > 0 holds); border
+            // words defer the whole decision to the replacement pass.
+            const uint32_t cand = (rows_ok && !col_border) ? (flagged & lt_bits(card, rep4(125u))) : flagged;
+            *reinterpret_cast<uint32_t*>(dstb + y * kRP + 4 * w) = win[BETA][BETA];
+            // bits 7,15,23,31 -> nibble (no carries: the shifted copies never overlap)
+            cmap[y * kCompWords + (w - kFirstWord)] = static_cast<uint8_t>((cand * 0x00204081u) >> 28);
+            if ((y >= HALO) && (y < HALO + out_rows)) nfl[t] += __popc(flagged & own_col);
 #pragma unroll
             for (int i = 0; i < NB - 1; ++i)
 #pragma unroll
                 for (int j = 0; j < NB; ++j) win[i][j] = win[i + 1][j];
         }
-        if (t + 1 < T) __syncthreads();
+        __syncthreads();
+        // replacement pass: one warp per row, compact the row's candidates
+        // (16 px per lane, one warp scan) and process them 32 at a time.
+        {
+            const int warp = threadIdx.x >> 5;
+            const int rlo = BETA * (t + 1), rhi = sh - BETA * (t + 1);
+            for (int y = rlo + warp; y < rhi; y += kWarps) {
+                uint32_t m = *reinterpret_cast<const uint32_t*>(cmap + y * kCompWords + 4 * lane);
+                const int n = __popc(m);
+                int incl = n;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const int v = __shfl_up_sync(0xffffffffu, incl, d);
+                    if (lane >= d) incl += v;
+                }
+                const int total = __shfl_sync(0xffffffffu, incl, 31);
+                if (total == 0) continue;
+                int pos = incl - n;
+                while (m) {
+                    const int b = __ffs(m) - 1;
+                    m &= m - 1;
+                    list[pos++] = static_cast<uint16_t>(4 * (kFirstWord + 4 * lane + (b >> 3)) + (b & 7));
+                }
+                __syncwarp();
+                for (int i = lane; i < total; i += 32)
+                    nrp[t] += process_pixel<BETA>(y, list[i], src, dstb, x0, gy0, HALO, HALO + out_rows, a);
+                __syncwarp();
+            }
+        }
+        __syncthreads();
+    }
+
+    // owned output rows: shared -> global, 16-byte coalesced stores
+    {
+        const uint8_t* fin = buf[T & 1];
+        constexpr int kOutChunks = kOutPx / 16;  // 31
+        uint8_t* gbase = a.dst + img * a.image_stride + static_cast<int64_t>(y0) * a.pitch + (x0 + kLeftPx);
+        for (int i = threadIdx.x; i < out_rows * kOutChunks; i += kThreads) {
+            const int r = i / kOutChunks, ch = i - r * kOutChunks;
+            if (x0 + kLeftPx + 16 * ch >= a.width) continue;
+            const int y = HALO + r;
+            const uint4 v = *reinterpret_cast<const uint4*>(fin + y * kRP + kLeftPx + 16 * ch);
+            *reinterpret_cast<uint4*>(gbase + static_cast<int64_t>(y) * a.pitch + 16 * ch) = v;
+        }
     }
 
     // counters: warp reduce -> smem -> one global atomic per CTA per value
@@ -323,7 +362,7 @@ __global__ void __launch_bounds__(kThreads)
     for (int t = 0; t < T; ++t) {
         const unsigned f = __reduce_add_sync(0xffffffffu, nfl[t]);
         const unsigned r = __reduce_add_sync(0xffffffffu, nrp[t]);
-        if ((threadIdx.x & 31) == 0) {
+        if (lane == 0) {
             if (f) atomicAdd(&red[t][0], f);
             if (r) atomicAdd(&red[t][1], r);
         }

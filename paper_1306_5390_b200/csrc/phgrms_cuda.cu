@@ -76,7 +76,9 @@ int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::once_flag g_encode_once;
 
-int encode_map(CUtensorMap* map, const phg_dev_image& im, int box_cols, int box_rows) {
+// The image is viewed as [images][rows][chunks][16 px] so that one 4-D box
+// {16, 33, SH, 1} lands as a dense [SH][528] shared tile (kernels.cuh).
+int encode_map(CUtensorMap* map, const phg_dev_image& im, int box_rows) {
     std::call_once(g_encode_once, [] {
         cudaDriverEntryPointQueryResult q;
         void* fn = nullptr;
@@ -88,15 +90,16 @@ int encode_map(CUtensorMap* map, const phg_dev_image& im, int box_cols, int box_
     if (!g_encode) return fail(PHG_ENODEV, "cuTensorMapEncodeTiled unavailable");
     if ((reinterpret_cast<uintptr_t>(im.data) & 15) || (im.pitch & 15) || (im.image_stride & 15))
         return fail(PHG_EINVAL, "device image must be 16-byte aligned with 16-byte pitches");
-    cuuint64_t dims[3] = {static_cast<cuuint64_t>(im.width), static_cast<cuuint64_t>(im.rows),
+    if (im.pitch < round_up(im.width, 16)) return fail(PHG_EINVAL, "pitch must be >= width rounded up to 16");
+    const int64_t chunks = round_up(im.width, 16) / 16;
+    cuuint64_t dims[4] = {16, static_cast<cuuint64_t>(chunks), static_cast<cuuint64_t>(im.rows),
                           static_cast<cuuint64_t>(im.n_images)};
-    cuuint64_t strides[2] = {static_cast<cuuint64_t>(im.pitch),
+    cuuint64_t strides[3] = {16, static_cast<cuuint64_t>(im.pitch),
                              static_cast<cuuint64_t>(im.n_images > 1 ? im.image_stride
                                                                      : im.pitch * im.rows)};
-    if (strides[1] == 0) strides[1] = 16;
-    cuuint32_t box[3] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows), 1};
-    cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, im.data, dims, strides, box, estr,
+    cuuint32_t box[4] = {16, static_cast<cuuint32_t>(phg::kChunks), static_cast<cuuint32_t>(box_rows), 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, im.data, dims, strides, box, estr,
                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(PHG_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
@@ -104,7 +107,7 @@ int encode_map(CUtensorMap* map, const phg_dev_image& im, int box_cols, int box_
 }
 
 // ------------------------------------------------------ kernel dispatch
-using FusedFn = void (*)(const CUtensorMap, const CUtensorMap, const phg::TileArgs);
+using FusedFn = void (*)(const CUtensorMap, const phg::TileArgs);
 
 template <int B, int T, bool A>
 FusedFn fused_ptr() {
@@ -130,7 +133,7 @@ struct Launch {
 // Output rows per tile: keep the staged region near 64 rows while not
 // wasting rows on a ragged last tile.
 Launch plan_rows(int own_rows, int halo) {
-    const int target = std::max(8, 64 - 2 * halo);
+    const int target = std::max(8, 56 - 2 * halo);
     const int tiles = std::max(1, (own_rows + target - 1) / target);
     const int th = (own_rows + tiles - 1) / tiles;
     return {th, (own_rows + th - 1) / th};
@@ -144,11 +147,10 @@ int launch_fused(const phg_dev_image& src, const phg_dev_image& dst, int row_bas
     const int halo = p.beta * iters;
     const Launch L = plan_rows(own_hi - own_lo, halo);
     const int sh = L.th + 2 * halo;
-    const size_t smem = 2ull * phg::buf_bytes(sh);
+    const size_t smem = phg::smem_bytes(sh);
     if (sh > 256) return fail(PHG_EINVAL, "tile too tall");
-    CUtensorMap map, apron;
-    PHG_TRY(encode_map(&map, src, phg::kHalfPx, sh));
-    PHG_TRY(encode_map(&apron, src, phg::kApronBox, sh));
+    CUtensorMap map;
+    PHG_TRY(encode_map(&map, src, sh));
     PHG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     phg::TileArgs a;
@@ -173,19 +175,18 @@ int launch_fused(const phg_dev_image& src, const phg_dev_image& dst, int row_bas
     for (int z0 = 0; z0 < src.n_images; z0 += 65535) {
         const int nz = std::min(65535, src.n_images - z0);
         // images beyond the first chunk: offset the tensor map and pointers
-        CUtensorMap m2 = map, ap2 = apron;
+        CUtensorMap m2 = map;
         phg::TileArgs a2 = a;
         if (z0) {
             phg_dev_image s2 = src;
             s2.data += z0 * src.image_stride;
             s2.n_images = nz;
-            PHG_TRY(encode_map(&m2, s2, phg::kHalfPx, sh));
-            PHG_TRY(encode_map(&ap2, s2, phg::kApronBox, sh));
+            PHG_TRY(encode_map(&m2, s2, sh));
             a2.dst += z0 * dst.image_stride;
             a2.counters += static_cast<int64_t>(z0) * kcap * 2;
         }
         dim3 grid(tiles_x, L.tiles_y, nz);
-        fn<<<grid, phg::kThreads, smem, stream>>>(m2, ap2, a2);
+        fn<<<grid, phg::kThreads, smem, stream>>>(m2, a2);
         ++g_launches;
         PHG_CUDA(cudaGetLastError());
     }
