@@ -14,6 +14,7 @@
 #pragma once
 #include <cuda.h>
 #include <cstdint>
+#include <type_traits>
 
 #include "swar.cuh"
 
@@ -157,45 +158,35 @@ __device__ __forceinline__ uint32_t rms_round32(uint32_t S, uint32_t f) {
 }
 
 // One candidate pixel: decide and compute the RMS replacement exactly as
-// removal_rows (denoise.hpp:192-217).  Returns 1 if it is an owned pixel
-// that was replaced (for the per-iteration counters).
+// removal_rows (denoise.hpp:192-217).  Cells outside the image hold 0 in the
+// staged tile, so they add nothing to the sum of squares and count as
+// dissimilar exactly when p >= alpha; the in-bounds count corrects f.
+// Returns 1 if an owned pixel was replaced (per-iteration counters).
 template <int BETA>
 __device__ __forceinline__ uint32_t process_pixel(int y, int px, const uint8_t* src, uint8_t* dst,
                                                   int gx0, int gy0, int own_y_lo, int own_y_hi,
                                                   const TileArgs& a) {
+    constexpr int W2 = (2 * BETA + 1) * (2 * BETA + 1);
     const uint8_t* c = src + y * kRP + px;
     const int p = *c;
+    uint32_t S = 0, fc = 0;
+#pragma unroll
+    for (int dy = -BETA; dy <= BETA; ++dy)
+#pragma unroll
+        for (int dx = -BETA; dx <= BETA; ++dx) {
+            if (dy == 0 && dx == 0) continue;
+            const uint32_t q = c[dy * kRP + dx];
+            const bool dis = __vabsdiffu4(q, static_cast<uint32_t>(p)) >= static_cast<uint32_t>(a.alpha);
+            S += dis ? q * q : 0u;
+            fc += dis;
+        }
     const int gr = gy0 + y, gc = gx0 + px;
-    uint32_t S = 0, f = 0;
-    int pix_count;
-    if (gr >= BETA && gr < a.height - BETA && gc >= BETA && gc < a.width - BETA) {
-#pragma unroll
-        for (int dy = -BETA; dy <= BETA; ++dy)
-#pragma unroll
-            for (int dx = -BETA; dx <= BETA; ++dx) {
-                if (dy == 0 && dx == 0) continue;
-                const int q = c[dy * kRP + dx];
-                const bool dis = abs(q - p) >= a.alpha;
-                S += dis ? static_cast<uint32_t>(q * q) : 0u;
-                f += dis;
-            }
-        pix_count = (2 * BETA + 1) * (2 * BETA + 1);
-    } else {
-        int inb = 0;
-        for (int dy = -BETA; dy <= BETA; ++dy)
-            for (int dx = -BETA; dx <= BETA; ++dx) {
-                const int rr = gr + dy, cc = gc + dx;
-                if (rr < 0 || rr >= a.height || cc < 0 || cc >= a.width) continue;
-                ++inb;
-                const int q = c[dy * kRP + dx];
-                const bool dis = abs(q - p) >= a.alpha;
-                S += dis ? static_cast<uint32_t>(q * q) : 0u;
-                f += dis;
-            }
-        pix_count = a.faithful ? (2 * BETA + 1) * (2 * BETA + 1) : inb;
-    }
-    if (static_cast<int>(f) > pix_count - 3 && f > 0) {
-        dst[y * kRP + px] = static_cast<uint8_t>(rms_round32(S, f));
+    const int inb = (min(gr + BETA, a.height - 1) - max(gr - BETA, 0) + 1) *
+                    (min(gc + BETA, a.width - 1) - max(gc - BETA, 0) + 1);
+    const int f = static_cast<int>(fc) - (p >= a.alpha ? W2 - inb : 0);
+    const int pix_count = a.faithful ? W2 : inb;
+    if (f > pix_count - 3 && f > 0) {
+        dst[y * kRP + px] = static_cast<uint8_t>(rms_round32(S, static_cast<uint32_t>(f)));
         return (y >= own_y_lo && y < own_y_hi && px >= kLeftPx && px < kLeftPx + kOutPx && gc < a.width) ? 1u
                                                                                                          : 0u;
     }
@@ -249,6 +240,7 @@ __global__ void __launch_bounds__(kThreads)
         colm[j] = m;
     }
     const uint32_t inimg_col = colm[BETA];
+    const uint32_t inimg_bytes = msb_to_bytes(inimg_col);  // 0xff per in-image lane
     const bool own_word = (w >= kOutWordLo) && (w < kOutWordHi);
     const uint32_t own_col = own_word ? inimg_col : 0u;
     const bool col_border = (gcol - BETA < 0) || (gcol + 3 + BETA > a.width - 1);
@@ -259,6 +251,17 @@ __global__ void __launch_bounds__(kThreads)
 
     __syncthreads();  // barrier init + counters visible
     mbar_wait(&bar, 0);
+    {
+        // The TMA box reads the whole 16-px chunk that holds column W-1; its
+        // bytes past the image edge are pitch padding, not zeros.  Clear them
+        // so every cell outside the image is 0 in the staged tile.
+        const int zlo = a.width - x0, zhi = min((a.width + 15) / 16 * 16 - x0, kRP);
+        if (zlo >= 0 && zlo < zhi) {
+            const int nz = zhi - zlo;
+            for (int i = threadIdx.x; i < sh * nz; i += kThreads) buf[0][(i / nz) * kRP + zlo + i % nz] = 0;
+            __syncthreads();
+        }
+    }
 
     const int g_lo = g * sh / kGroups;
     const int g_hi = (g + 1) * sh / kGroups;
@@ -275,42 +278,46 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
             for (int i = 0; i < NB - 1; ++i) load_row<BETA>(colp + (ylo - BETA + i) * kRP, win[i]);
         }
-        for (int y = ylo; y < yhi; ++y) {
+        // rows with the whole window inside the image need no row masks
+        const int yint_lo = min(max(ylo, BETA - gy0), yhi);
+        const int yint_hi = max(min(yhi, a.height - BETA - gy0), yint_lo);
+        uint32_t fl_acc = 0;  // per-lane flagged counts (bytes; < 256 rows per thread)
+        auto row = [&](int y, auto rows_ok_tag) {
+            constexpr bool ROWS_OK = decltype(rows_ok_tag)::value;
             load_row<BETA>(colp + (y + BETA) * kRP, win[NB - 1]);
-            const int gr = gy0 + y;  // global row
-            const bool rows_ok = (gr - BETA >= 0) && (gr + BETA < a.height);
-            uint32_t cnt;
-            if (rows_ok) {
-                uint32_t rowm[NB];
+            const int gr = gy0 + y;
+            uint32_t rowm[NB];
+            bool row_in = true;
 #pragma unroll
-                for (int i = 0; i < NB; ++i) rowm[i] = 0xffffffffu;
-                cnt = count_similar<BETA, ALE, true>(win, colm, rowm, a.k7);
-            } else {
-                uint32_t rowm[NB];
-#pragma unroll
-                for (int i = 0; i < NB; ++i) {
-                    const int rr = gr + i - BETA;
-                    rowm[i] = (rr >= 0 && rr < a.height) ? 0xffffffffu : 0u;
-                }
-                cnt = count_similar<BETA, ALE, false>(win, colm, rowm, a.k7);
+            for (int i = 0; i < NB; ++i) {
+                const int rr = gr + i - BETA;
+                rowm[i] = ROWS_OK || (rr >= 0 && rr < a.height) ? 0xffffffffu : 0u;
             }
+            if (!ROWS_OK) row_in = rowm[BETA] != 0;
+            const uint32_t cnt = count_similar<BETA, ALE, ROWS_OK>(win, colm, rowm, a.k7);
             const uint32_t card = cnt + 0x01010101u;
-            const bool row_in = (gr >= 0) && (gr < a.height);
             const uint32_t inimg = row_in ? inimg_col : 0u;
             const uint32_t flagged = lt_bits(card, a.k_thr) & inimg;
             // interior: in_bounds = pix_count = (2B+1)^2, so
             // flag > pix_count-3 <=> card < 3 (and flag > 0 holds); border
             // words defer the whole decision to the replacement pass.
-            const uint32_t cand = (rows_ok && !col_border) ? (flagged & lt_bits(card, rep4(125u))) : flagged;
-            *reinterpret_cast<uint32_t*>(dstb + y * kRP + 4 * w) = win[BETA][BETA];
+            const uint32_t cand = (ROWS_OK && !col_border) ? (flagged & lt_bits(card, rep4(125u))) : flagged;
+            // pixels outside the image are kept at 0 (see process_pixel)
+            *reinterpret_cast<uint32_t*>(dstb + y * kRP + 4 * w) =
+                win[BETA][BETA] & (row_in ? inimg_bytes : 0u);
             // bits 7,15,23,31 -> nibble (no carries: the shifted copies never overlap)
             cmap[y * kCompWords + (w - kFirstWord)] = static_cast<uint8_t>((cand * 0x00204081u) >> 28);
-            if ((y >= HALO) && (y < HALO + out_rows)) nfl[t] += __popc(flagged & own_col);
+            if (y >= HALO && y < HALO + out_rows) fl_acc += (flagged & own_col) >> 7;
 #pragma unroll
             for (int i = 0; i < NB - 1; ++i)
 #pragma unroll
                 for (int j = 0; j < NB; ++j) win[i][j] = win[i + 1][j];
-        }
+        };
+        for (int y = ylo; y < yint_lo; ++y) row(y, std::false_type{});
+#pragma unroll 3
+        for (int y = yint_lo; y < yint_hi; ++y) row(y, std::true_type{});
+        for (int y = yint_hi; y < yhi; ++y) row(y, std::false_type{});
+        nfl[t] += __dp4a(fl_acc, 0x01010101u, 0u);
         __syncthreads();
         // replacement pass: one warp per row, compact the row's candidates
         // (16 px per lane, one warp scan) and process them 32 at a time.

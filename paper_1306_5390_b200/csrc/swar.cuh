@@ -37,6 +37,14 @@ __device__ __forceinline__ uint32_t lt_bits(uint32_t c, uint32_t k_thr) {
 
 __device__ __forceinline__ uint32_t rep4(uint32_t b) { return b * 0x01010101u; }
 
+// 0xff in every byte whose bit 7 is set (PRMT sign-replicate mode; note that
+// the __byte_perm intrinsic masks the selector's replicate bit away).
+__device__ __forceinline__ uint32_t msb_to_bytes(uint32_t x) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, 0, 0xba98;" : "=r"(r) : "r"(x));
+    return r;
+}
+
 // round-half-away-from-zero of sqrt(S/f), exactly as the reference's
 // llround(sqrt(double(S)/f)) (denoise.hpp:163-169): u is the largest
 // integer with u - 1/2 <= sqrt(S/f), i.e. (2u-1)^2 * f <= 4S (u >= 1), or 0.
