@@ -56,6 +56,9 @@ def lib():
         L.orc_denoise.argtypes = [_u8p, C.c_int, C.c_int, C.POINTER(_Params), _u8p, _i64p, _i64p,
                                   C.POINTER(C.c_int)]
         L.orc_row_blocks.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.orc_band_pass.argtypes = [_u8p, _u8p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                    C.c_int, C.c_int, C.POINTER(_Params), C.POINTER(C.c_int64),
+                                    C.POINTER(C.c_int64)]
         L.orc_mt19937_nth.argtypes = [C.c_uint32, C.c_uint64]
         L.orc_mt19937_nth.restype = C.c_uint32
         _LIB = L
@@ -156,6 +159,18 @@ def denoise(img, alpha=20, beta=1, k=5, thr=3, border=0):
     p = _params(alpha, beta, k, thr, border)
     assert lib().orc_denoise(img, w, h, C.byref(p), out, fl, rp, C.byref(it)) == 0
     return out, [(int(fl[i]), int(rp[i])) for i in range(it.value)]
+
+
+def band_pass(src, dst, row_base, height, y_lo, y_hi, c_lo, c_hi, alpha=20, beta=1, thr=3, border=0):
+    """One iteration on a band buffer (see orc_band_pass); returns (flagged, replaced)."""
+    rows, w = src.shape
+    f, r = C.c_int64(), C.c_int64()
+    p = _params(alpha, beta, 1, thr, border)
+    rc = lib().orc_band_pass(src, dst, w, rows, row_base, height, y_lo, y_hi, c_lo, c_hi, C.byref(p),
+                             C.byref(f), C.byref(r))
+    if rc != 0:
+        raise ValueError(f"band_pass: band does not hold the rows it needs (rc={rc})")
+    return f.value, r.value
 
 
 def row_blocks(height, workers):

@@ -319,3 +319,56 @@ int orc_row_blocks(int height, int workers, int* begins, int* ends) {
     }
     return nb;
 }
+
+/* One iteration on a row band held in a buffer (the global-coordinate form
+ * of cardinality_rows + removal_rows, denoise.hpp:139-160 / 176-223).
+ * Buffer row b holds global image row b + row_base of an image `height`
+ * rows tall.  Global rows [y_lo, y_hi) are computed into dst (same layout);
+ * flagged/replaced are counted only over global rows [c_lo, c_hi).  Window
+ * cells outside the IMAGE are excluded exactly as in the reference; the
+ * caller guarantees every in-image row within beta of [y_lo, y_hi) is held
+ * by the buffer.  Test infrastructure for the multi-rank band exchange. */
+int orc_band_pass(const uint8_t* src, uint8_t* dst, int w, int buf_rows, int row_base, int height,
+                  int y_lo, int y_hi, int c_lo, int c_hi, const orc_params* p, int64_t* flagged,
+                  int64_t* replaced) {
+    if (orc_validate(p)) return -1;
+    const int full_window = (2 * p->beta + 1) * (2 * p->beta + 1);
+    int64_t nf = 0, nr = 0;
+    for (int r = y_lo; r < y_hi; ++r) {
+        const int r0 = r - p->beta < 0 ? 0 : r - p->beta;
+        const int r1 = r + p->beta > height - 1 ? height - 1 : r + p->beta;
+        if (r0 - row_base < 0 || r1 - row_base >= buf_rows) return -2;
+        for (int c = 0; c < w; ++c) {
+            const int c0 = c - p->beta < 0 ? 0 : c - p->beta;
+            const int c1 = c + p->beta > w - 1 ? w - 1 : c + p->beta;
+            const int center = src[(size_t)(r - row_base) * w + c];
+            int card = 0, flag = 0;
+            uint64_t sum_sq = 0;
+            for (int i = r0; i <= r1; ++i)
+                for (int j = c0; j <= c1; ++j) {
+                    const int v = src[(size_t)(i - row_base) * w + j];
+                    if (similar(v, center, p->alpha))
+                        ++card;
+                    else {
+                        sum_sq += (uint64_t)v * (uint64_t)v;
+                        ++flag;
+                    }
+                }
+            uint8_t value = (uint8_t)center;
+            const int counted = r >= c_lo && r < c_hi;
+            if (card < p->card_threshold) {
+                nf += counted;
+                const int in_bounds = (r1 - r0 + 1) * (c1 - c0 + 1);
+                const int pix_count = p->border == 0 ? full_window : in_bounds;
+                if (flag > pix_count - 3 && flag > 0) {
+                    value = (uint8_t)orc_rms_replacement(sum_sq, flag);
+                    nr += counted;
+                }
+            }
+            dst[(size_t)(r - row_base) * w + c] = value;
+        }
+    }
+    *flagged = nf;
+    *replaced = nr;
+    return 0;
+}

@@ -1,0 +1,117 @@
+#!/usr/bin/env python
+"""Regenerate the golden fixtures from the REFERENCE ITSELF.
+
+Runs the reference's header-only C++ library (compiled in place from
+/root/reference/proj/include by oracle/Makefile into
+oracle/_ref/libphgrms_ref.so) on seeded inputs and stores its outputs:
+
+  small_cases.npz   ~80 small random cases: input, iteration-1 cardinality
+                    map, one removal pass, the final denoise image and the
+                    per-iteration (flagged, replaced) stats
+  digests.json      SHA-256 digests + stats for the BASELINE configs
+                    (C1 481x321, C2 3840x2160, a C4 subset, a beta=2 crop)
+
+The fixtures are committed; this script only needs to run again if the
+reference changes.  It is the only thing here that needs /root/reference.
+"""
+import hashlib
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+from oracle import oracle as O  # noqa: E402
+
+assert O.ref_available(), "build oracle/_ref first (make -C oracle)"
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def small_cases():
+    rng = np.random.default_rng(1306_5390)
+    cases = []
+    for i in range(80):
+        w, h = int(rng.integers(1, 41)), int(rng.integers(1, 41))
+        alpha = int(rng.choice([1, 2, 10, 20, 20, 20, 37, 60, 128, 129, 200, 255]))
+        beta = int(rng.choice([1, 1, 1, 2, 2, 3]))
+        thr = int(rng.choice([1, 2, 3, 3, 3, 5, 30]))
+        border = int(rng.integers(0, 2))
+        k = int(rng.choice([1, 5, 5, 8]))
+        if i % 3 == 0:
+            img = rng.integers(0, 256, (h, w), dtype=np.uint8)
+        else:
+            img = O.ref_inject_sp_noise(O.ref_synth_image(w, h, int(rng.integers(0, 2**31))),
+                                        float(rng.uniform(0.0, 0.8)), 0.5, int(rng.integers(0, 2**31)))
+        card = O.ref_cardinality(img, alpha, beta)
+        R = O.ref()
+        out1 = np.empty_like(img)
+        import ctypes as C
+        f1, r1 = C.c_int64(), C.c_int64()
+        assert R.ref_denoise_pass(img, card, w, h, alpha, beta, k, thr, border, 1, out1,
+                                  C.byref(f1), C.byref(r1)) == 0
+        fin, stats = O.ref_denoise(img, alpha, beta, k, thr, border)
+        cases.append(dict(w=w, h=h, alpha=alpha, beta=beta, thr=thr, border=border, k=k, img=img, card=card,
+                          pass_out=out1, pass_stats=(f1.value, r1.value), final=fin, stats=stats))
+    flat = {}
+    meta = []
+    for i, c in enumerate(cases):
+        for key in ("img", "card", "pass_out", "final"):
+            flat[f"{key}_{i}"] = c[key]
+        meta.append({k: c[k] for k in ("w", "h", "alpha", "beta", "thr", "border", "k", "pass_stats", "stats")})
+    flat["meta"] = np.frombuffer(json.dumps(meta).encode(), np.uint8)
+    np.savez_compressed(os.path.join(HERE, "small_cases.npz"), **flat)
+    return len(cases)
+
+
+def c4_density(i):
+    return 0.10 + 0.60 * (i % 61) / 60
+
+
+def digests():
+    out = {}
+    # C1: BSDS size, 10%, beta=1 (k=5 and k=64)
+    clean = O.ref_synth_image(481, 321, 1)
+    noisy = O.ref_inject_sp_noise(clean, 0.10, 0.5, 12345)
+    fin, st = O.ref_denoise(noisy)
+    fin64, st64 = O.ref_denoise(noisy, k=64)
+    out["c1"] = dict(w=481, h=321, clean_seed=1, density=0.10, noise_seed=12345, beta=1, clean=sha(clean),
+                     noisy=sha(noisy), card1=sha(O.ref_cardinality(noisy, 20, 1)), final=sha(fin), stats=st,
+                     final_k64=sha(fin64), stats_k64=st64)
+    # C2: 4K, 30%, beta=1
+    clean = O.ref_synth_image(3840, 2160, 1)
+    noisy = O.ref_inject_sp_noise(clean, 0.30, 0.5, 12345)
+    fin, st = O.ref_denoise(noisy, workers=8)
+    out["c2"] = dict(w=3840, h=2160, clean_seed=1, density=0.30, noise_seed=12345, beta=1, noisy=sha(noisy),
+                     card1=sha(O.ref_cardinality(noisy, 20, 1, workers=8)), final=sha(fin), stats=st)
+    # C3 crop: 2048^2 at 50%, beta=2 (the full 16384^2 is checked by properties)
+    clean = O.ref_synth_image(2048, 2048, 1)
+    noisy = O.ref_inject_sp_noise(clean, 0.50, 0.5, 12345)
+    fin, st = O.ref_denoise(noisy, beta=2, workers=8)
+    out["c3_2048"] = dict(w=2048, h=2048, clean_seed=1, density=0.50, noise_seed=12345, beta=2,
+                          noisy=sha(noisy), final=sha(fin), stats=st)
+    # C4: the first 16 images of the batch stream
+    imgs = []
+    for i in range(16):
+        imgs.append(dict(i=i, density=c4_density(i)))
+        n = O.ref_inject_sp_noise(O.ref_synth_image(481, 321, i), c4_density(i), 0.5, i)
+        fin, st = O.ref_denoise(n)
+        imgs[-1].update(noisy=sha(n), final=sha(fin), stats=st)
+    out["c4_first16"] = imgs
+    # SURVEY KATs: constant-128 + 1% noise stops at iteration 3
+    n = O.ref_inject_sp_noise(np.full((321, 481), 128, np.uint8), 0.01, 0.5, 7)
+    fin, st = O.ref_denoise(n)
+    out["flat_1pct"] = dict(noisy=sha(n), final=sha(fin), stats=st)
+    with open(os.path.join(HERE, "digests.json"), "w") as f:
+        json.dump(out, f, indent=1)
+
+
+if __name__ == "__main__":
+    print("small cases:", small_cases())
+    digests()
+    print("ok")
