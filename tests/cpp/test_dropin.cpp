@@ -1,0 +1,166 @@
+// The reference's hot-path unit tests (proj/tests/test_denoise.cpp and
+// test_parallel.cpp), restated as plain checks and compiled against the
+// drop-in headers in include/phgrms/ -- i.e. code written for the reference
+// API, unchanged, now running on the B200 kernels.  Built by
+// __graft_entry__.build(); run by tests/test_dropin_gpu.py on a GPU.
+#include <cstdio>
+#include <random>
+#include <stdexcept>
+
+#include "phgrms/denoise.hpp"
+#include "phgrms/image.hpp"
+#include "phgrms/noise.hpp"
+
+using namespace phgrms;
+
+static int g_fail = 0, g_checks = 0;
+#define CHECK(x)                                                              \
+    do {                                                                      \
+        ++g_checks;                                                           \
+        if (!(x)) {                                                           \
+            ++g_fail;                                                         \
+            std::fprintf(stderr, "%s:%d CHECK failed: %s\n", __FILE__, __LINE__, #x); \
+        }                                                                     \
+    } while (0)
+#define CHECK_THROWS_AS(expr, ex)    \
+    do {                             \
+        bool thrown_ = false;        \
+        try {                        \
+            (void)(expr);            \
+        } catch (const ex&) {        \
+            thrown_ = true;          \
+        }                            \
+        CHECK(thrown_);              \
+    } while (0)
+
+static GrayImage random_image(std::mt19937& rng, int w, int h) {
+    GrayImage img(w, h);
+    for (auto& p : img.pixels) p = static_cast<std::uint8_t>(rng() & 0xFF);
+    return img;
+}
+
+int main() {
+    {  // cardinality of a constant image equals the in-bounds window size
+        const auto card = compute_cardinality(GrayImage(3, 3, 100), 20, 1);
+        CHECK((card.counts == std::vector<std::int32_t>{4, 6, 4, 6, 9, 6, 4, 6, 4}));
+    }
+    {  // cardinality isolates a centre impulse
+        GrayImage img(3, 3, 100);
+        img.at(1, 1) = 255;
+        CHECK((compute_cardinality(img, 20, 1).counts == std::vector<std::int32_t>{3, 5, 3, 5, 1, 5, 3, 5, 3}));
+        const auto [out, st] = denoise_pass(img, compute_cardinality(img, 20, 1), DenoiseParams{});
+        CHECK(out == GrayImage(3, 3, 100));
+        CHECK(st.flagged == 1 && st.replaced == 1);
+    }
+    {  // border mode forks the corner behaviour
+        GrayImage img(4, 4, 50);
+        img.at(0, 0) = 255;
+        const auto card = compute_cardinality(img, 20, 1);
+        CHECK(card.at(0, 0) == 1);
+        const auto [kept, ks] = denoise_pass(img, card, DenoiseParams{});
+        CHECK(kept == img && ks.flagged == 1 && ks.replaced == 0);
+        DenoiseParams inb;
+        inb.border = BorderMode::InBounds;
+        const auto [fixed, fs] = denoise_pass(img, card, inb);
+        CHECK(fixed == GrayImage(4, 4, 50) && fs.replaced == 1);
+    }
+    {  // two adjacent impulses clear in pass 1 and stop in pass 2
+        GrayImage img(7, 7, 100);
+        img.at(3, 3) = img.at(3, 4) = 255;
+        const auto r = denoise(img, DenoiseParams{});
+        CHECK(r.image == GrayImage(7, 7, 100));
+        CHECK(r.stats.size() == 2 && r.stats[0].replaced == 2 && r.stats[1].replaced == 0);
+    }
+    {  // driver stops after one clean pass on a constant image
+        const auto r = denoise(GrayImage(64, 64, 77), DenoiseParams{});
+        CHECK(r.stats.size() == 1 && r.stats[0].iteration == 1 && r.stats[0].replaced == 0);
+    }
+    {  // an isolated interior impulse is restored exactly in one pass
+        std::mt19937 rng(105);
+        for (int i = 0; i < 30; ++i) {
+            const int v = static_cast<int>(rng() % 256);
+            DenoiseParams p;
+            p.alpha = 1 + static_cast<int>(rng() % 100);
+            const int imp = static_cast<int>(rng() % 256);
+            if (std::abs(imp - v) < p.alpha) continue;
+            GrayImage img(5, 5, static_cast<std::uint8_t>(v));
+            img.at(2, 2) = static_cast<std::uint8_t>(imp);
+            const auto r = denoise(img, p);
+            CHECK(r.stats.front().replaced == 1);
+            CHECK(r.image == GrayImage(5, 5, static_cast<std::uint8_t>(v)));
+        }
+    }
+    {  // faithful borders never rewrite beta=1 corners; C >= thr untouched
+        std::mt19937 rng(104);
+        for (int i = 0; i < 20; ++i) {
+            const GrayImage img = random_image(rng, 7, 7);
+            DenoiseParams p;
+            p.alpha = 1 + static_cast<int>(rng() % 255);
+            const auto card = compute_cardinality(img, p.alpha, p.beta);
+            const auto [out, st] = denoise_pass(img, card, p);
+            for (int r : {0, 6})
+                for (int c : {0, 6}) CHECK(out.at(r, c) == img.at(r, c));
+            for (std::size_t j = 0; j < img.size(); ++j)
+                if (card.counts[j] >= p.card_threshold) CHECK(out.pixels[j] == img.pixels[j]);
+            CHECK(st.replaced <= st.flagged);
+        }
+    }
+    {  // parallel output is bit-identical to serial for any worker count
+        std::mt19937 rng(201);
+        for (int i = 0; i < 25; ++i) {
+            const GrayImage img = random_image(rng, 1 + static_cast<int>(rng() % 32), 1 + static_cast<int>(rng() % 32));
+            DenoiseParams p;
+            p.alpha = 1 + static_cast<int>(rng() % 60);
+            p.beta = 1 + static_cast<int>(rng() % 2);
+            p.border = (rng() & 1) ? BorderMode::InBounds : BorderMode::Faithful;
+            const auto serial = denoise(img, p, EngineSpec::serial());
+            for (const int w : {2, 3, 8}) {
+                const auto par = denoise(img, p, EngineSpec::parallel(w));
+                CHECK(par.image == serial.image);
+                CHECK(par.stats.size() == serial.stats.size());
+                for (std::size_t s = 0; s < par.stats.size() && s < serial.stats.size(); ++s)
+                    CHECK(par.stats[s].flagged == serial.stats[s].flagged &&
+                          par.stats[s].replaced == serial.stats[s].replaced);
+            }
+        }
+    }
+    {  // a zero-replacement pass is a fixed point
+        std::mt19937 rng(106);
+        for (int i = 0; i < 10; ++i) {
+            const GrayImage img = random_image(rng, 12, 12);
+            DenoiseParams p;
+            p.alpha = 1 + static_cast<int>(rng() % 120);
+            p.max_iterations = 8;
+            const auto r = denoise(img, p);
+            if (r.stats.back().replaced == 0) {
+                const auto [again, st] = denoise_pass(r.image, compute_cardinality(r.image, p.alpha, p.beta), p);
+                CHECK(again == r.image && st.replaced == 0);
+            }
+        }
+    }
+    {  // parameter validation + rms rounding + row blocks
+        const GrayImage img(4, 4, 1);
+        DenoiseParams p;
+        p.alpha = 0;
+        CHECK_THROWS_AS(denoise(img, p), std::invalid_argument);
+        p = {};
+        p.beta = 0;
+        CHECK_THROWS_AS(denoise(img, p), std::invalid_argument);
+        p = {};
+        p.max_iterations = 0;
+        CHECK_THROWS_AS(denoise(img, p), std::invalid_argument);
+        CHECK_THROWS_AS(denoise_pass(img, compute_cardinality(GrayImage(3, 3, 1), 20, 1), DenoiseParams{}),
+                        std::invalid_argument);
+        using detail::rms_replacement;
+        CHECK(rms_replacement(0, 1) == 0 && rms_replacement(2, 1) == 1 && rms_replacement(9, 4) == 2);
+        CHECK(rms_replacement(25, 4) == 3 && rms_replacement(65025ULL, 1) == 255 &&
+              rms_replacement(65025ULL * 8, 8) == 255);
+        CHECK(row_blocks(5, 8).size() == 5);
+    }
+    {  // noise fixture (test_noise.cpp:43-62) through the drop-in generator
+        const auto [noisy, mask] = inject_sp_noise(GrayImage(10, 10, 100), {0.2, 0.5, 77});
+        CHECK(noisy.pixels[4] == 255 && noisy.pixels[2] == 0 && mask.count() == 20);
+    }
+    std::printf("dropin: %d checks, %d failures\n", g_checks, g_fail);
+    return g_fail ? 1 : 0;
+}
