@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libphgrms_cuda.so")
+LIB_PATH = os.environ.get("PHG_LIB_PATH") or os.path.join(HERE, "libphgrms_cuda.so")
 
 PHG_OK, PHG_EINVAL, PHG_ECUDA, PHG_ENOMEM, PHG_ENODEV = 0, -1, -2, -3, -4
 

@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "../../include/phgrms_b200.h"
+#include "kernel_b1.cuh"
 #include "kernels.cuh"
 
 namespace {
@@ -125,6 +126,30 @@ FusedFn select_fused(int beta, int T, bool ale) {
 
 int max_fused(int beta) { return beta == 1 ? 5 : beta == 2 ? 4 : 0; }
 
+using B1Fn = void (*)(const CUtensorMap, const phg::TileArgs, const uint32_t);
+
+template <int T, bool A>
+B1Fn b1_ptr() {
+    return phg::fused_b1_kernel<T, A>;
+}
+
+B1Fn select_b1(int T, bool ale) {
+#define PHG_CASE(TT) \
+    if (T == TT) return ale ? b1_ptr<TT, true>() : b1_ptr<TT, false>();
+    PHG_CASE(1) PHG_CASE(2) PHG_CASE(3) PHG_CASE(4) PHG_CASE(5)
+#undef PHG_CASE
+    return nullptr;
+}
+
+// staged rows per tile for the beta=1 kernel (tunable: PHG_B1_ROWS)
+int b1_rows_target() {
+    static const int v = [] {
+        const char* e = getenv("PHG_B1_ROWS");
+        return e ? std::max(16, std::min(200, atoi(e))) : 58;
+    }();
+    return v;
+}
+
 struct Launch {
     int th;
     int tiles_y;
@@ -132,8 +157,8 @@ struct Launch {
 
 // Output rows per tile: keep the staged region near 64 rows while not
 // wasting rows on a ragged last tile.
-Launch plan_rows(int own_rows, int halo) {
-    const int target = std::max(8, 56 - 2 * halo);
+Launch plan_rows(int own_rows, int halo, int rows_target) {
+    const int target = std::max(8, rows_target - 2 * halo);
     const int tiles = std::max(1, (own_rows + target - 1) / target);
     const int th = (own_rows + tiles - 1) / tiles;
     return {th, (own_rows + th - 1) / th};
@@ -142,16 +167,18 @@ Launch plan_rows(int own_rows, int halo) {
 int launch_fused(const phg_dev_image& src, const phg_dev_image& dst, int row_base, int height,
                  int own_lo, int own_hi, const phg_params& p, int it0, int iters,
                  uint64_t* counters, int kcap, cudaStream_t stream) {
-    FusedFn fn = select_fused(p.beta, iters, p.alpha <= 128);
-    if (!fn) return fail(PHG_EINVAL, "no fused kernel for this beta / iteration count");
+    const bool b1 = p.beta == 1 && getenv("PHG_B1_SYM");  // opt-in: see DESIGN.md (slower on B200)
+    FusedFn fn = b1 ? nullptr : select_fused(p.beta, iters, p.alpha <= 128);
+    B1Fn fn1 = b1 ? select_b1(iters, p.alpha <= 128) : nullptr;
+    if (!fn && !fn1) return fail(PHG_EINVAL, "no fused kernel for this beta / iteration count");
     const int halo = p.beta * iters;
-    const Launch L = plan_rows(own_hi - own_lo, halo);
+    const Launch L = plan_rows(own_hi - own_lo, halo, b1 ? b1_rows_target() : 56);
     const int sh = L.th + 2 * halo;
-    const size_t smem = phg::smem_bytes(sh);
+    const size_t smem = b1 ? phg::b1_smem_bytes(sh) : phg::smem_bytes(sh);
     if (sh > 256) return fail(PHG_EINVAL, "tile too tall");
     CUtensorMap map;
     PHG_TRY(encode_map(&map, src, sh));
-    PHG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+    PHG_CUDA(cudaFuncSetAttribute(b1 ? reinterpret_cast<const void*>(fn1) : reinterpret_cast<const void*>(fn),
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     phg::TileArgs a;
     a.dst = dst.data;
@@ -171,6 +198,7 @@ int launch_fused(const phg_dev_image& src, const phg_dev_image& dst, int row_bas
     a.it0 = it0;
     a.kcap = kcap;
     a.counters = reinterpret_cast<unsigned long long*>(counters);
+    a.one = 1u;
     const int tiles_x = (src.width + phg::kOutPx - 1) / phg::kOutPx;
     for (int z0 = 0; z0 < src.n_images; z0 += 65535) {
         const int nz = std::min(65535, src.n_images - z0);
@@ -186,7 +214,10 @@ int launch_fused(const phg_dev_image& src, const phg_dev_image& dst, int row_bas
             a2.counters += static_cast<int64_t>(z0) * kcap * 2;
         }
         dim3 grid(tiles_x, L.tiles_y, nz);
-        fn<<<grid, phg::kThreads, smem, stream>>>(m2, a2);
+        if (b1)
+            fn1<<<grid, phg::kB1Threads, smem, stream>>>(m2, a2, 1u);
+        else
+            fn<<<grid, phg::kThreads, smem, stream>>>(m2, a2);
         ++g_launches;
         PHG_CUDA(cudaGetLastError());
     }
