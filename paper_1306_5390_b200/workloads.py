@@ -64,3 +64,40 @@ def single_image(key: str) -> np.ndarray:
     density = {"c1": 0.10, "c2": 0.30, "c3": 0.50}[key]
     clean = synth_image(wl.width, wl.height, 1)
     return inject_sp_noise(clean, NoiseSpec(density, 0.5, 12345)).pixels
+
+
+# ----------------------------------------------------------- C5 giga-pixel
+C5_SIZE = 65536
+C5_TILE = 4096
+
+
+def c5_tile(ti: int, tj: int, tile: int = C5_TILE) -> np.ndarray:
+    """Tile (ti, tj) of the C5 image.  The reference's inject_sp_noise draws
+    bounded_rand(uint32(total - i)), which divides by zero at 2^32 pixels
+    (SURVEY.md section 2), so the giga-pixel input is built per 4096^2 tile
+    with the reference's own generators: synth_image(SmoothRandom, seed
+    1 + 16*ti + tj) + inject_sp_noise(30%, salt 0.5, seed 12345 + 16*ti + tj).
+    Documented as a new generator; tile seams are ordinary image
+    content for the denoiser."""
+    k = 16 * ti + tj
+    clean = synth_image(tile, tile, 1 + k)
+    return inject_sp_noise(clean, NoiseSpec(0.30, 0.5, 12345 + k)).pixels
+
+
+def c5_rows(lo: int, hi: int, size: int = C5_SIZE, tile: int = C5_TILE, out: np.ndarray = None,
+            threads: int = None) -> np.ndarray:
+    """Global rows [lo, hi) of the C5 image (generated tile by tile)."""
+    if out is None:
+        out = np.empty((hi - lo, size), np.uint8)
+    threads = threads or min(32, os.cpu_count() or 1)
+    jobs = [(ti, tj) for ti in range(lo // tile, (hi - 1) // tile + 1) for tj in range(size // tile)]
+
+    def one(job):
+        ti, tj = job
+        t = c5_tile(ti, tj, tile)
+        r0, r1 = max(lo, ti * tile), min(hi, (ti + 1) * tile)
+        out[r0 - lo:r1 - lo, tj * tile:(tj + 1) * tile] = t[r0 - ti * tile:r1 - ti * tile]
+
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(one, jobs))
+    return out
