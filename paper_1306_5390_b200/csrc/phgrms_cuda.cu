@@ -297,10 +297,47 @@ std::vector<int> chunk_plan(int k, int beta) {
     return c;
 }
 
+// ------------------------------------------------- layout conversion kernels
+// Host images are unpadded ([n][h][w]); the fused kernel needs 16-byte
+// pitched rows (TMA).  Copying through the copy engine with cudaMemcpy2D and
+// w-byte rows is slow for narrow images (481 B rows), so the public API
+// moves contiguous bytes over PCIe and re-pitches on the device.
+__global__ void __launch_bounds__(256) pitch_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
+                                                    int w, int64_t pitch, int64_t rows, int to_pitched) {
+    const int words = (w + 3) >> 2;
+    const int64_t total = rows * words;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = i / words;
+        const int c = static_cast<int>(i - r * words) * 4;
+        const uint8_t* s = to_pitched ? src + r * w + c : src + r * pitch + c;
+        uint8_t* d = to_pitched ? dst + r * pitch + c : dst + r * w + c;
+        const int nb = min(4, w - c);
+        if (to_pitched && nb == 4) {
+            const uint32_t v = s[0] | (s[1] << 8) | (s[2] << 16) | (static_cast<uint32_t>(s[3]) << 24);
+            *reinterpret_cast<uint32_t*>(d) = v;
+        } else {
+            for (int k = 0; k < nb; ++k) d[k] = s[k];
+        }
+    }
+}
+
+int launch_pitch(const uint8_t* src, uint8_t* dst, int w, int64_t pitch, int64_t rows, bool to_pitched,
+                 cudaStream_t st) {
+    const int64_t words = rows * ((w + 3) / 4);
+    const int blocks = static_cast<int>(std::min<int64_t>((words + 255) / 256, 148 * 16));
+    pitch_kernel<<<std::max(1, blocks), 256, 0, st>>>(src, dst, w, pitch, rows, to_pitched ? 1 : 0);
+    ++g_launches;
+    PHG_CUDA(cudaGetLastError());
+    return PHG_OK;
+}
+
 // ------------------------------------------------------- per-device state
 struct DeviceState {
     cudaStream_t stream = nullptr;
+    cudaStream_t pipe[3] = {nullptr, nullptr, nullptr};  // chunked host<->device pipeline
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t pev[3] = {nullptr, nullptr, nullptr};
     std::vector<std::pair<void*, size_t>> bufs;  // grow-only scratch slots
 };
 
@@ -317,6 +354,10 @@ int current_state(DeviceState** out, int* dev_out = nullptr) {
         PHG_CUDA(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
         PHG_CUDA(cudaEventCreate(&s.ev0));
         PHG_CUDA(cudaEventCreate(&s.ev1));
+        for (int i = 0; i < 3; ++i) {
+            PHG_CUDA(cudaStreamCreateWithFlags(&s.pipe[i], cudaStreamNonBlocking));
+            PHG_CUDA(cudaEventCreateWithFlags(&s.pev[i], cudaEventDisableTiming));
+        }
     }
     *out = &s;
     if (dev_out) *dev_out = dev;
@@ -663,20 +704,41 @@ int phg_denoise_batch(const uint8_t* imgs, int n, int w, int h, const phg_params
     DeviceState* s;
     PHG_TRY(current_state(&s));
     const int k = p->max_iterations;
-    void *pi, *pa, *pb, *pk;
-    const phg_dev_image probe = make_image(nullptr, w, h, n);
-    const size_t bytes = static_cast<size_t>(probe.image_stride) * n;
-    PHG_TRY(scratch(s, 0, bytes, &pi));
-    PHG_TRY(scratch(s, 1, bytes, &pa));
-    PHG_TRY(scratch(s, 2, bytes, &pb));
+    // Chunked pipeline over three streams: contiguous H2D of chunk i+1 and
+    // D2H of chunk i-1 overlap the kernels of chunk i (host buffers should
+    // be pinned for the copies to be asynchronous).
+    const int nchunks = std::min(n, n >= 64 ? 8 : 1);
+    const int per = (n + nchunks - 1) / nchunks;
+    const int64_t pitch = round_up(w, 16);
+    const int64_t img_bytes = static_cast<int64_t>(w) * h, img_pitched = pitch * h;
+    void *pk, *slot_mem[3] = {nullptr, nullptr, nullptr};
+    const size_t slot_bytes = static_cast<size_t>(per) * (img_bytes + 3 * img_pitched) + 1024;
+    for (int i = 0; i < std::min(3, nchunks); ++i) PHG_TRY(scratch(s, 20 + i, slot_bytes, &slot_mem[i]));
     PHG_TRY(scratch(s, 4, sizeof(uint64_t) * 2 * k * n, &pk));
-    phg_dev_image im = make_image(pi, w, h, n), am = make_image(pa, w, h, n), bm = make_image(pb, w, h, n);
     uint64_t* ctr = static_cast<uint64_t*>(pk);
-    PHG_TRY(upload(im, imgs, s->stream));
     PHG_CUDA(cudaEventRecord(s->ev0, s->stream));
-    PHG_TRY(phg_dev_denoise(&im, &am, &bm, p, ctr, s->stream));
+    for (int i = 0; i < 3; ++i) PHG_CUDA(cudaStreamWaitEvent(s->pipe[i], s->ev0, 0));
+    for (int c = 0; c < nchunks; ++c) {
+        const int i0 = c * per, m = std::min(per, n - i0);
+        if (m <= 0) break;
+        cudaStream_t st = s->pipe[c % 3];
+        uint8_t* base = static_cast<uint8_t*>(slot_mem[c % 3]);
+        uint8_t* stage = base;  // contiguous [m][h][w]
+        uint8_t* pin = base + ((static_cast<int64_t>(per) * img_bytes + 255) / 256 * 256);
+        phg_dev_image im = make_image(pin, w, h, m);
+        phg_dev_image am = make_image(pin + img_pitched * per, w, h, m);
+        phg_dev_image bm = make_image(pin + 2 * img_pitched * per, w, h, m);
+        PHG_CUDA(cudaMemcpyAsync(stage, imgs + img_bytes * i0, img_bytes * m, cudaMemcpyHostToDevice, st));
+        PHG_TRY(launch_pitch(stage, im.data, w, pitch, static_cast<int64_t>(h) * m, true, st));
+        PHG_TRY(phg_dev_denoise(&im, &am, &bm, p, ctr + static_cast<int64_t>(2) * k * i0, st));
+        PHG_TRY(launch_pitch(am.data, stage, w, pitch, static_cast<int64_t>(h) * m, false, st));
+        PHG_CUDA(cudaMemcpyAsync(out + img_bytes * i0, stage, img_bytes * m, cudaMemcpyDeviceToHost, st));
+    }
+    for (int i = 0; i < 3; ++i) {
+        PHG_CUDA(cudaEventRecord(s->pev[i], s->pipe[i]));
+        PHG_CUDA(cudaStreamWaitEvent(s->stream, s->pev[i], 0));
+    }
     PHG_CUDA(cudaEventRecord(s->ev1, s->stream));
-    PHG_TRY(download(out, am, s->stream));
     std::vector<uint64_t> hc(static_cast<size_t>(2) * k * n);
     PHG_CUDA(cudaMemcpyAsync(hc.data(), ctr, sizeof(uint64_t) * hc.size(), cudaMemcpyDeviceToHost, s->stream));
     PHG_CUDA(cudaStreamSynchronize(s->stream));
