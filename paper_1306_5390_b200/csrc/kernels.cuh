@@ -37,6 +37,12 @@
 #ifndef PHG_LIST_OFFCHAIN
 #define PHG_LIST_OFFCHAIN 1
 #endif
+#ifndef PHG_REPL_OWN
+#define PHG_REPL_OWN 0
+#endif
+#ifndef PHG_VSYM
+#define PHG_VSYM 1
+#endif
 #ifndef PHG_FMA_ADD
 #define PHG_FMA_ADD 1
 #endif
@@ -68,14 +74,14 @@ constexpr int kGroups = 2;                  // row groups per CTA
 constexpr int kThreads = kCompWords * kGroups;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxHaloPx = 8;
-constexpr int kListCap = kCompWords * 4;    // per-warp candidate list (one row)
+constexpr int kRing = 64 + kCompWords * 4;  // per-warp candidate ring: < 64 pending + one row
 
 // bytes of one staged buffer of sh rows (rounded for 128-B alignment)
 __host__ __device__ constexpr int buf_bytes(int sh) { return (kRP * sh + 127) / 128 * 128; }
 // two staged buffers + candidate bitmap (one nibble-byte per word and row)
 // + per-warp candidate lists
 __host__ __device__ constexpr int smem_bytes(int sh) {
-    return 2 * buf_bytes(sh) + (kCompWords * sh + 127) / 128 * 128 + kWarps * kListCap * 2;
+    return 2 * buf_bytes(sh) + (kCompWords * sh + 127) / 128 * 128 + kWarps * kRing * 2;
 }
 
 struct TileArgs {
@@ -180,6 +186,17 @@ __device__ __forceinline__ uint32_t count_similar(const uint32_t (&win)[2 * BETA
     }
     return cnt;
 }
+
+// Vertical pair symmetry: the same-column pair (y, y+d) is tested once, at
+// row y ("down", returned) and reused as the "up" neighbour of row y+d.
+// up[d-1] must hold the mask of the pair (y-d, y); validity of a stored pair
+// already includes both rows and the column.
+template <int BETA, bool ALE, bool ROWS_OK>
+__device__ __forceinline__ uint32_t count_similar_vs(const uint32_t (&win)[2 * BETA + 1][2 * BETA + 1],
+                                                     const uint32_t (&colm)[2 * BETA + 1],
+                                                     const uint32_t (&rowm)[2 * BETA + 1], uint32_t k7,
+                                                     uint32_t one, const uint32_t (&up)[BETA],
+                                                     uint32_t (&down)[BETA]);
 
 // round(sqrt(S/f)) half away from zero, exact for S <= 2^24 / 4, f <= 2^10:
 // r ~ sqrt(4S/f) (few-ulp estimate); the answer floor((sqrt(4S/f)+1)/2)
@@ -319,6 +336,35 @@ __device__ __forceinline__ uint32_t process_b1(int y, int px, uint32_t interior,
     return 0;
 }
 
+template <int BETA, bool ALE, bool ROWS_OK>
+__device__ __forceinline__ uint32_t count_similar_vs(const uint32_t (&win)[2 * BETA + 1][2 * BETA + 1],
+                                                     const uint32_t (&colm)[2 * BETA + 1],
+                                                     const uint32_t (&rowm)[2 * BETA + 1], uint32_t k7,
+                                                     uint32_t one, const uint32_t (&up)[BETA],
+                                                     uint32_t (&down)[BETA]) {
+    const uint32_t p = win[BETA][BETA];
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int i = 0; i < 2 * BETA + 1; ++i) {
+#pragma unroll
+        for (int j = 0; j < 2 * BETA + 1; ++j) {
+            if (i == BETA && j == BETA) continue;
+            if (j == BETA && i < BETA) {
+                cnt += up[BETA - i - 1] >> 7;  // (y-d, y) tested at row y-d
+                continue;
+            }
+            uint32_t valid = ROWS_OK ? colm[j] : (colm[j] & rowm[i]);
+            if (j == BETA && i > BETA && !ROWS_OK) valid &= rowm[BETA];  // stored for row y+d
+            const uint32_t d = __vabsdiffu4(p, win[i][j]);
+            const uint32_t tt = fma_add(d & kLo7, one, k7);
+            const uint32_t sm = valid & ~(ALE ? (d | tt) : (d & tt));
+            if (j == BETA && i > BETA) down[i - BETA - 1] = sm;
+            cnt += sm >> 7;
+        }
+    }
+    return cnt;
+}
+
 template <int BETA, int T, bool ALE>
 __global__ void __launch_bounds__(kThreads)
     fused_tb_kernel(const __grid_constant__ CUtensorMap src_map, const TileArgs a) {
@@ -335,7 +381,7 @@ __global__ void __launch_bounds__(kThreads)
     const int lane = threadIdx.x & 31;
     uint8_t* cmap = smem + 2 * buf_bytes(sh);  // [sh][128] candidate nibbles
     uint16_t* list = reinterpret_cast<uint16_t*>(cmap + (kCompWords * sh + 127) / 128 * 128) +
-                     (threadIdx.x >> 5) * kListCap;
+                     (threadIdx.x >> 5) * kRing;
 
     const int img = blockIdx.z;
     const int x0 = blockIdx.x * kOutPx - kLeftPx;  // global col of region px 0 (16-aligned)
@@ -410,6 +456,31 @@ __global__ void __launch_bounds__(kThreads)
         const int yint_lo = min(max(ylo, BETA - gy0), yhi);
         const int yint_hi = max(min(yhi, a.height - BETA - gy0), yint_lo);
         uint32_t fl_acc = 0, rp_acc = 0;  // per-lane counts (bytes; < 256 rows per thread)
+        uint32_t cb0 = 0, cb1 = 0, cb2 = 0, cb3 = 0;  // candidate shift register (PHG_REPL_OWN)
+#if PHG_VSYM
+        // same-column pairs for the first rows: up[d-1] = (ylo-d, ylo);
+        // pend[d-2][q] = (ylo+1+q-d, ylo+1+q) for rows ylo+1+q, q < d-1
+        uint32_t up[BETA];
+        uint32_t pend[BETA > 1 ? BETA - 1 : 1][BETA > 1 ? BETA - 1 : 1];
+        if (ylo < yhi) {
+            auto rv = [&](int yy) { const int g = gy0 + yy; return (g >= 0 && g < a.height) ? 0xffffffffu : 0u; };
+#pragma unroll
+            for (int d = 1; d <= BETA; ++d) {
+                const uint32_t da = __vabsdiffu4(win[BETA][BETA], win[BETA - d][BETA]);
+                const uint32_t ta = fma_add(da & kLo7, a.one, a.k7);
+                up[d - 1] = colm[BETA] & rv(ylo) & rv(ylo - d) & ~(ALE ? (da | ta) : (da & ta));
+            }
+#pragma unroll
+            for (int d = 2; d <= BETA; ++d)
+#pragma unroll
+                for (int q = 0; q < d - 1; ++q) {
+                    // rows ylo+1+q and ylo+1+q-d are window rows BETA+1+q and BETA+1+q-d (< NB-1)
+                    const uint32_t db = __vabsdiffu4(win[BETA + 1 + q][BETA], win[BETA + 1 + q - d][BETA]);
+                    const uint32_t tb = fma_add(db & kLo7, a.one, a.k7);
+                    pend[d - 2][q] = colm[BETA] & rv(ylo + 1 + q) & rv(ylo + 1 + q - d) & ~(ALE ? (db | tb) : (db & tb));
+                }
+        }
+#endif
         auto row = [&](int y, auto rows_ok_tag) {
             constexpr bool ROWS_OK = decltype(rows_ok_tag)::value;
             load_row<BETA>(colp + (y + BETA) * kRP, win[NB - 1]);
@@ -422,7 +493,24 @@ __global__ void __launch_bounds__(kThreads)
                 rowm[i] = ROWS_OK || (rr >= 0 && rr < a.height) ? 0xffffffffu : 0u;
             }
             if (!ROWS_OK) row_in = rowm[BETA] != 0;
+#if PHG_VSYM
+            uint32_t down[BETA];
+            const uint32_t cnt = count_similar_vs<BETA, ALE, ROWS_OK>(win, colm, rowm, a.k7, a.one, up, down);
+            // rotate the pending same-column pairs: up[d-1] for row y+1
+#pragma unroll
+            for (int d = BETA; d >= 2; --d) up[d - 1] = pend[d - 2][0];
+            if (BETA >= 2) {
+#pragma unroll
+                for (int d = 2; d <= BETA; ++d) {
+#pragma unroll
+                    for (int q = 0; q < d - 2; ++q) pend[d - 2][q] = pend[d - 2][q + 1];
+                    pend[d - 2][d - 2] = down[d - 1];
+                }
+            }
+            up[0] = down[0];
+#else
             const uint32_t cnt = count_similar<BETA, ALE, ROWS_OK>(win, colm, rowm, a.k7, a.one);
+#endif
             const uint32_t card = cnt + 0x01010101u;
             const uint32_t inimg = row_in ? inimg_col : 0u;
             const uint32_t flagged = lt_bits(card, a.k_thr) & inimg;
@@ -436,9 +524,21 @@ __global__ void __launch_bounds__(kThreads)
             *reinterpret_cast<uint32_t*>(dstb + y * kRP + 4 * w) =
                 win[BETA][BETA] & (row_in ? inimg_bytes : 0u);
             // bits 7,15,23,31 -> nibble (no carries: the shifted copies never overlap)
+#if PHG_REPL_OWN
+            // this thread's own candidates: 4 bits per row pushed into a
+            // 128-bit shift register (rows per group <= 32)
+            {
+                const uint32_t nib = (cand * 0x00204081u) >> 28;
+                cb3 = __funnelshift_l(cb2, cb3, 4);
+                cb2 = __funnelshift_l(cb1, cb2, 4);
+                cb1 = __funnelshift_l(cb0, cb1, 4);
+                cb0 = (cb0 << 4) | nib;
+            }
+#else
             // + bit 4: the word's candidates are decided interior replacements
             cmap[y * kCompWords + (w - kFirstWord)] =
                 static_cast<uint8_t>(((cand * 0x00204081u) >> 28) | (kTag && interior ? 0x10u : 0u));
+#endif
             if (y >= HALO && y < HALO + out_rows) {
                 fl_acc += (flagged & own_col) >> 7;
                 if (kTag && interior) rp_acc += (cand & own_col) >> 7;
@@ -454,74 +554,112 @@ __global__ void __launch_bounds__(kThreads)
         for (int y = yint_hi; y < yhi; ++y) row(y, std::false_type{});
         nfl[t] += __dp4a(fl_acc, 0x01010101u, 0u);
         nrp[t] += __dp4a(rp_acc, 0x01010101u, 0u);
+#if PHG_REPL_OWN
+        // replacement by the thread that swept the word: no compaction; the
+        // warp runs as long as its busiest lane (src is immutable and every
+        // candidate pixel belongs to exactly one thread, so no barrier is needed
+        // before the end of the step)
+        __syncwarp();
+        if (ylo < yhi) {
+            const int nrows = yhi - ylo;
+            uint32_t cbs[4] = {cb0, cb1, cb2, cb3};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                uint32_t m = cbs[k];
+                while (m) {
+                    const uint32_t lb = m & (0u - m);
+                    m ^= lb;
+                    const int P = 32 * k + __popc(lb - 1u);  // bit position in the 128-bit register
+                    const int y = ylo + nrows - 1 - (P >> 2);
+                    const int px = 4 * w + (P & 3);
+                    if (BETA == 1 && PHG_PROC_SWAR)
+                        nrp[t] += process_b1<ALE>(y, px, 0u, src, dstb, x0, gy0, HALO, HALO + out_rows, a, a.one, rcp);
+                    else
+                        nrp[t] += process_pixel<BETA>(y, px, 0u, src, dstb, x0, gy0, HALO, HALO + out_rows, a);
+                }
+            }
+        }
         __syncthreads();
-        // replacement pass: one warp per row, compact the row's candidates
-        // (16 px per lane, one ballot prefix) and process them 32 at a time.
+#else
+        __syncthreads();
+        // replacement pass.  Each warp takes rows rlo+warp, +kWarps, ...; a
+        // row's candidates (16 px per lane) are compacted with one warp scan
+        // into the warp's ring of u16 items (y << 10 | px).  Items carry over
+        // between rows, and the ring is drained only in full rounds of 64 --
+        // two independent candidates per lane, so both dependency chains
+        // (window loads -> sum of squares -> RMS) are in flight together.
         {
             const int warp = threadIdx.x >> 5;
             const int rlo = BETA * (t + 1), rhi = sh - BETA * (t + 1);
+            int head = 0, pending = 0;  // warp-uniform ring state
+            auto item_px = [&](uint32_t it, uint32_t& r) {
+                const int yy = it >> 10, px = it & 1023;
+                if (BETA == 1 && PHG_PROC_SWAR)
+                    r = process_b1<ALE>(yy, px, 0u, src, dstb, x0, gy0, HALO, HALO + out_rows, a, a.one, rcp);
+                else
+                    r = process_pixel<BETA>(yy, px, 0u, src, dstb, x0, gy0, HALO, HALO + out_rows, a);
+            };
+            auto drain = [&](int n) {  // process n <= 64 items starting at head
+                int i0 = head + lane, i1 = head + lane + 32;
+                if (i0 >= kRing) i0 -= kRing;
+                if (i1 >= kRing) i1 -= kRing;
+                const bool ok0 = lane < n, ok1 = lane + 32 < n;
+                const uint32_t it0 = list[ok0 ? i0 : head], it1 = list[ok1 ? i1 : head];
+                uint32_t r0, r1;
+                if (n == 64) {
+                    item_px(it0, r0);
+                    item_px(it1, r1);
+                } else {
+                    r0 = r1 = 0;
+                    if (ok0) item_px(it0, r0);
+                    if (ok1) item_px(it1, r1);
+                }
+                nrp[t] += r0 + r1;
+                head += n;
+                if (head >= kRing) head -= kRing;
+                pending -= n;
+            };
 #if PHG_DBG_NO_REPL
             if (true) {} else
 #endif
             for (int y = rlo + warp; y < rhi; y += kWarps) {
-                const uint32_t e = *reinterpret_cast<const uint32_t*>(cmap + y * kCompWords + 4 * lane);
-                uint32_t m = e & 0x0f0f0f0fu;
+                uint32_t m = *reinterpret_cast<const uint32_t*>(cmap + y * kCompWords + 4 * lane) & 0x0f0f0f0fu;
                 const int n = __popc(m);
-                int excl = 0, total = 0;
-#if PHG_SCAN_BALLOT
-                const unsigned lt = (1u << lane) - 1u;
-#pragma unroll
-                for (int k = 0; k < 5; ++k) {
-                    const unsigned bb = __ballot_sync(0xffffffffu, (n >> k) & 1);
-                    excl += __popc(bb & lt) << k;
-                    total += __popc(bb) << k;
-                }
-#else
                 int incl = n;
 #pragma unroll
                 for (int d = 1; d < 32; d <<= 1) {
                     const int v = __shfl_up_sync(0xffffffffu, incl, d);
                     if (lane >= d) incl += v;
                 }
-                total = __shfl_sync(0xffffffffu, incl, 31);
-                excl = incl - n;
-#endif
+                const int total = __shfl_sync(0xffffffffu, incl, 31);
                 if (total == 0) continue;
-                int pos = excl;
+                int pos = head + pending + incl - n;
+                if (pos >= kRing) pos -= kRing;
                 while (m) {
-#if PHG_INTERIOR_TAG
-                    const int b = 31 - __clz(m);
-                    m ^= 1u << b;
-                    const uint32_t intr = (e >> ((b & ~7) + 4)) & 1u;
-#elif PHG_LIST_OFFCHAIN
                     // loop-carried chain is two ALU ops; the bit index (XU) is off it
                     const uint32_t lb = m & (0u - m);
                     m ^= lb;
                     const int b = __popc(lb - 1u);
-                    const uint32_t intr = 0;
-#else
-                    const int b = __ffs(m) - 1;
-                    m &= m - 1;
-                    const uint32_t intr = 0;
-#endif
-                    list[pos++] = static_cast<uint16_t>((intr << 15) | (4 * (kFirstWord + 4 * lane + (b >> 3)) + (b & 7)));
+                    list[pos] = static_cast<uint16_t>((y << 10) | (4 * (kFirstWord + 4 * lane + (b >> 3)) + (b & 7)));
+                    if (++pos == kRing) pos = 0;
                 }
+                pending += total;
                 __syncwarp();
 #if PHG_DBG_NO_PROCESS
-                if (true) continue;
+                head += pending;
+                head %= kRing;
+                pending = 0;
+                continue;
 #endif
-                for (int i = lane; i < total; i += 32) {
-                    const uint32_t it = list[i];
-                    if (BETA == 1 && PHG_PROC_SWAR)
-                        nrp[t] += process_b1<ALE>(y, it & 0x7fff, it >> 15, src, dstb, x0, gy0, HALO,
-                                                  HALO + out_rows, a, a.one, rcp);
-                    else
-                        nrp[t] += process_pixel<BETA>(y, it & 0x7fff, it >> 15, src, dstb, x0, gy0, HALO,
-                                                      HALO + out_rows, a);
-                }
+                while (pending >= 64) drain(64);
                 __syncwarp();
             }
+            while (pending > 0) {
+                __syncwarp();
+                drain(min(pending, 64));
+            }
         }
+#endif
         __syncthreads();
     }
 

@@ -141,6 +141,15 @@ B1Fn select_b1(int T, bool ale) {
     return nullptr;
 }
 
+// staged rows per tile for the generic kernel (tunable: PHG_ROWS)
+int generic_rows_target() {
+    static const int v = [] {
+        const char* e = getenv("PHG_ROWS");
+        return e ? std::max(16, std::min(200, atoi(e))) : 56;
+    }();
+    return v;
+}
+
 // staged rows per tile for the beta=1 kernel (tunable: PHG_B1_ROWS)
 int b1_rows_target() {
     static const int v = [] {
@@ -172,10 +181,11 @@ int launch_fused(const phg_dev_image& src, const phg_dev_image& dst, int row_bas
     B1Fn fn1 = b1 ? select_b1(iters, p.alpha <= 128) : nullptr;
     if (!fn && !fn1) return fail(PHG_EINVAL, "no fused kernel for this beta / iteration count");
     const int halo = p.beta * iters;
-    const Launch L = plan_rows(own_hi - own_lo, halo, b1 ? b1_rows_target() : 56);
+    const Launch L = plan_rows(own_hi - own_lo, halo, b1 ? b1_rows_target() : generic_rows_target());
     const int sh = L.th + 2 * halo;
     const size_t smem = b1 ? phg::b1_smem_bytes(sh) : phg::smem_bytes(sh);
     if (sh > 256) return fail(PHG_EINVAL, "tile too tall");
+    if (!b1 && sh > 64) return fail(PHG_EINVAL, "tile too tall for the candidate register (<= 32 rows per group)");
     CUtensorMap map;
     PHG_TRY(encode_map(&map, src, sh));
     PHG_CUDA(cudaFuncSetAttribute(b1 ? reinterpret_cast<const void*>(fn1) : reinterpret_cast<const void*>(fn),
