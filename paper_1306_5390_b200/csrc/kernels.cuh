@@ -74,7 +74,7 @@ constexpr int kGroups = 2;                  // row groups per CTA
 constexpr int kThreads = kCompWords * kGroups;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxHaloPx = 8;
-constexpr int kRing = 64 + kCompWords * 4;  // per-warp candidate ring: < 64 pending + one row
+constexpr int kRing = 64 + kCompWords * 4;  // per-warp candidate list: < 64 leftovers + one row
 
 // bytes of one staged buffer of sh rows (rounded for 128-B alignment)
 __host__ __device__ constexpr int buf_bytes(int sh) { return (kRP * sh + 127) / 128 * 128; }
@@ -591,7 +591,7 @@ __global__ void __launch_bounds__(kThreads)
         {
             const int warp = threadIdx.x >> 5;
             const int rlo = BETA * (t + 1), rhi = sh - BETA * (t + 1);
-            int head = 0, pending = 0;  // warp-uniform ring state
+            int pending = 0;  // warp-uniform: items waiting at list[0, pending)
             auto item_px = [&](uint32_t it, uint32_t& r) {
                 const int yy = it >> 10, px = it & 1023;
                 if (BETA == 1 && PHG_PROC_SWAR)
@@ -599,12 +599,10 @@ __global__ void __launch_bounds__(kThreads)
                 else
                     r = process_pixel<BETA>(yy, px, 0u, src, dstb, x0, gy0, HALO, HALO + out_rows, a);
             };
-            auto drain = [&](int n) {  // process n <= 64 items starting at head
-                int i0 = head + lane, i1 = head + lane + 32;
-                if (i0 >= kRing) i0 -= kRing;
-                if (i1 >= kRing) i1 -= kRing;
+            // process list[h, h+n), n <= 64: two independent items per lane
+            auto drain = [&](int h, int n) {
                 const bool ok0 = lane < n, ok1 = lane + 32 < n;
-                const uint32_t it0 = list[ok0 ? i0 : head], it1 = list[ok1 ? i1 : head];
+                const uint32_t it0 = list[h + (ok0 ? lane : 0)], it1 = list[h + (ok1 ? lane + 32 : 0)];
                 uint32_t r0, r1;
                 if (n == 64) {
                     item_px(it0, r0);
@@ -615,15 +613,15 @@ __global__ void __launch_bounds__(kThreads)
                     if (ok1) item_px(it1, r1);
                 }
                 nrp[t] += r0 + r1;
-                head += n;
-                if (head >= kRing) head -= kRing;
-                pending -= n;
             };
 #if PHG_DBG_NO_REPL
             if (true) {} else
 #endif
             for (int y = rlo + warp; y < rhi; y += kWarps) {
-                uint32_t m = *reinterpret_cast<const uint32_t*>(cmap + y * kCompWords + 4 * lane) & 0x0f0f0f0fu;
+                // this lane's 16 px (4 words x 4 lanes) as 16 contiguous bits
+                const uint32_t e = *reinterpret_cast<const uint32_t*>(cmap + y * kCompWords + 4 * lane) & 0x0f0f0f0fu;
+                const uint32_t e2 = e | (e >> 4);
+                uint32_t m = __byte_perm(e2, 0, 0x0020) & 0xffffu;  // bytes 0 and 2
                 const int n = __popc(m);
                 int incl = n;
 #pragma unroll
@@ -633,31 +631,34 @@ __global__ void __launch_bounds__(kThreads)
                 }
                 const int total = __shfl_sync(0xffffffffu, incl, 31);
                 if (total == 0) continue;
-                int pos = head + pending + incl - n;
-                if (pos >= kRing) pos -= kRing;
+                int pos = pending + incl - n;
+                const uint32_t base = (static_cast<uint32_t>(y) << 10) | (4 * (kFirstWord + 4 * lane));
                 while (m) {
                     // loop-carried chain is two ALU ops; the bit index (XU) is off it
                     const uint32_t lb = m & (0u - m);
                     m ^= lb;
-                    const int b = __popc(lb - 1u);
-                    list[pos] = static_cast<uint16_t>((y << 10) | (4 * (kFirstWord + 4 * lane + (b >> 3)) + (b & 7)));
-                    if (++pos == kRing) pos = 0;
+                    list[pos++] = static_cast<uint16_t>(base + __popc(lb - 1u));
                 }
                 pending += total;
                 __syncwarp();
 #if PHG_DBG_NO_PROCESS
-                head += pending;
-                head %= kRing;
                 pending = 0;
                 continue;
 #endif
-                while (pending >= 64) drain(64);
+                int h = 0;
+                for (; pending - h >= 64; h += 64) drain(h, 64);
+                pending -= h;
+                if (h && pending) {  // move the < 64 leftovers to the front
+                    __syncwarp();
+                    const uint16_t v = lane < pending ? list[h + lane] : 0;
+                    const uint16_t v2 = lane + 32 < pending ? list[h + lane + 32] : 0;
+                    __syncwarp();
+                    if (lane < pending) list[lane] = v;
+                    if (lane + 32 < pending) list[lane + 32] = v2;
+                }
                 __syncwarp();
             }
-            while (pending > 0) {
-                __syncwarp();
-                drain(min(pending, 64));
-            }
+            if (pending > 0) drain(0, pending);
         }
 #endif
         __syncthreads();
