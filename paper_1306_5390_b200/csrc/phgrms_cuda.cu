@@ -23,6 +23,7 @@
 
 #include "../../include/phgrms_b200.h"
 #include "kernel_b1.cuh"
+#include "kernel_h2.cuh"
 #include "kernels.cuh"
 
 namespace {
@@ -173,9 +174,98 @@ Launch plan_rows(int own_rows, int halo, int rows_target) {
     return {th, (own_rows + th - 1) / th};
 }
 
+using H2Fn = void (*)(const CUtensorMap, const phg::H2Args);
+
+template <int T, bool A>
+H2Fn h2_ptr() {
+    return phg::fused_h2_kernel<T, A>;
+}
+
+H2Fn select_h2(int T, bool ale) {
+#define PHG_CASE(TT) \
+    if (T == TT) return ale ? h2_ptr<TT, true>() : h2_ptr<TT, false>();
+    PHG_CASE(1) PHG_CASE(2) PHG_CASE(3) PHG_CASE(4) PHG_CASE(5)
+#undef PHG_CASE
+    return nullptr;
+}
+
+// staged rows per tile for the two-tile fp16 kernel (tunable: PHG_H2_ROWS);
+// 51 rows keep two CTAs (2 x 112.5 KB) resident per SM
+int h2_rows_target() {
+    static const int v = [] {
+        const char* e = getenv("PHG_H2_ROWS");
+        return e ? std::max(16, std::min(62, atoi(e))) : 46;
+    }();
+    return v;
+}
+
+// The fp16 two-tile kernel covers the reference defaults: beta = 1, Faithful
+// borders, card_threshold <= 3 (PHG_NO_H2=1 forces fused_tb_kernel).
+bool use_h2(const phg_params& p, int iters) {
+    static const bool off = getenv("PHG_NO_H2") != nullptr;
+    return !off && p.beta == 1 && p.border == PHG_BORDER_FAITHFUL && p.card_threshold <= 3 && iters <= 5;
+}
+
+uint16_t half_bits(float f) {
+    // exact for the small integers and halves used here
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    const uint32_t sign = (u >> 16) & 0x8000u;
+    const int e = static_cast<int>((u >> 23) & 0xff) - 127 + 15;
+    const uint32_t m = (u >> 13) & 0x3ffu;
+    if (f == 0.0f) return static_cast<uint16_t>(sign);
+    return static_cast<uint16_t>(sign | (static_cast<uint32_t>(e) << 10) | m);
+}
+
+int launch_h2(const phg_dev_image& src, const phg_dev_image& dst, int row_base, int height, int own_lo,
+              int own_hi, const phg_params& p, int it0, int iters, uint64_t* counters, int kcap,
+              cudaStream_t stream) {
+    H2Fn fn = select_h2(iters, p.alpha <= 128);
+    if (!fn) return fail(PHG_EINVAL, "no two-tile kernel for this iteration count");
+    const int halo = iters;
+    const Launch L = plan_rows(own_hi - own_lo, halo, h2_rows_target());
+    const int sh = L.th + 2 * halo;
+    if (sh > phg::kH2MaxRows) return fail(PHG_EINVAL, "tile too tall");
+    const size_t smem = phg::h2_smem_bytes(sh);
+    CUtensorMap map;
+    PHG_TRY(encode_map(&map, src, sh));
+    PHG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    phg::H2Args a;
+    a.dst = dst.data;
+    a.pitch = dst.pitch;
+    a.image_stride = dst.image_stride;
+    a.width = src.width;
+    a.height = height;
+    a.row_base = row_base;
+    a.own_lo = own_lo;
+    a.own_hi = own_hi;
+    a.th = L.th;
+    a.tiles_x = (src.width + phg::kOutPx - 1) / phg::kOutPx;
+    a.tiles_y = L.tiles_y;
+    const int64_t n_tiles = static_cast<int64_t>(src.n_images) * a.tiles_x * a.tiles_y;
+    if (n_tiles > (int64_t(1) << 31) - 2) return fail(PHG_EINVAL, "too many tiles for one launch");
+    a.n_tiles = static_cast<int>(n_tiles);
+    const uint32_t ah = half_bits(static_cast<float>(p.alpha));
+    a.alpha2 = ah | (ah << 16);
+    a.k7 = ((256u - static_cast<uint32_t>(p.alpha)) & 0x7fu) * 0x01010101u;
+    a.m = std::min(p.card_threshold - 2, 1);
+    a.thr = p.card_threshold;
+    a.it0 = it0;
+    a.kcap = kcap;
+    a.counters = reinterpret_cast<unsigned long long*>(counters);
+    const unsigned grid = static_cast<unsigned>((n_tiles + 1) / 2);
+    fn<<<grid, phg::kH2Threads, smem, stream>>>(map, a);
+    ++g_launches;
+    PHG_CUDA(cudaGetLastError());
+    return PHG_OK;
+}
+
 int launch_fused(const phg_dev_image& src, const phg_dev_image& dst, int row_base, int height,
                  int own_lo, int own_hi, const phg_params& p, int it0, int iters,
                  uint64_t* counters, int kcap, cudaStream_t stream) {
+    if (use_h2(p, iters))
+        return launch_h2(src, dst, row_base, height, own_lo, own_hi, p, it0, iters, counters, kcap, stream);
     const bool b1 = p.beta == 1 && getenv("PHG_B1_SYM");  // opt-in: see DESIGN.md (slower on B200)
     FusedFn fn = b1 ? nullptr : select_fused(p.beta, iters, p.alpha <= 128);
     B1Fn fn1 = b1 ? select_b1(iters, p.alpha <= 128) : nullptr;
