@@ -142,7 +142,7 @@ __device__ __forceinline__ void h2_pairs_down(const uint32_t (&v)[6], const uint
 __device__ __forceinline__ uint32_t h2_rms(uint32_t S, uint32_t f, float rcp_f) {
     const float s4 = __int_as_float(0x4b000000 | (4u * S)) - 8388608.0f;  // exact
     float r;
-    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(s4 * rcp_f));
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(s4 * rcp_f));
     const int m = max(__float_as_int(r + 12582912.0f) - 0x4b400000, 1);  // nearest (S = 0 -> 1 -> 0)
     const uint32_t u0 = static_cast<uint32_t>(m + 1) >> 1;
     const uint32_t q = 2u * u0 - 1u;
@@ -160,9 +160,10 @@ __device__ __forceinline__ uint32_t lds16(uint32_t addr) {
 
 // One candidate pixel (interior, Faithful, beta=1): RMS of the dissimilar
 // cells of its 3x3 window, exactly as removal_rows (denoise.hpp:199-217).
-// `o` = byte offset of the pixel in the interleaved tile.
+// `o` = byte offset of the pixel in the interleaved tile; returns the new
+// value (no store, so that two candidates' loads can be interleaved).
 template <bool ALE>
-__device__ __forceinline__ void h2_replace(const uint8_t* src, uint8_t* dst, int o, uint32_t k7) {
+__device__ __forceinline__ uint32_t h2_replace(const uint8_t* src, int o, uint32_t k7) {
     const int o1 = o - kH2RP - 2;
     const int b4 = o1 & ~3;
     const uint32_t sh = static_cast<uint32_t>(o1 & 3);
@@ -183,7 +184,7 @@ __device__ __forceinline__ void h2_replace(const uint8_t* src, uint8_t* dst, int
     const uint32_t f = __popc(dis1 | (dis2 >> 1));
     const uint32_t S = __dp4a(n2 & msb_to_bytes(dis2), n2, __dp4a(n1 & msb_to_bytes(dis1), n1, 0u));
     const float rcp = f == 8u ? 0.125f : 0.142857149f;  // f in {7, 8}
-    dst[o] = static_cast<uint8_t>(h2_rms(S, f, rcp));
+    return h2_rms(S, f, rcp);
 }
 
 template <int T, bool ALE>
@@ -324,20 +325,16 @@ __global__ void __launch_bounds__(kH2Threads, 2)
         // process ring[h, h+n), n <= 64: two independent candidates per lane
         auto drain = [&](int h, int n) {
             // item = quad << 10 | lane << 5 | bit (quad = first row / 4)
-            auto one = [&](uint32_t it) {
-                const int o = static_cast<int>(it >> 10) * (4 * kH2RP) + c_w + 8 * static_cast<int>((it >> 5) & 31) +
-                              otab[it & 31];
-                h2_replace<ALE>(src, dst, o, a.k7);
+            auto off = [&](uint32_t it) {
+                return static_cast<int>(it >> 10) * (4 * kH2RP) + c_w + 8 * static_cast<int>((it >> 5) & 31) +
+                       otab[it & 31];
             };
-            const uint32_t i0 = lds16(ring + 2 * (h + (lane < n ? lane : 0)));
-            const uint32_t i1 = lds16(ring + 2 * (h + (lane + 32 < n ? lane + 32 : 0)));
-            if (n == 64) {
-                one(i0);
-                one(i1);
-            } else {
-                if (lane < n) one(i0);
-                if (lane + 32 < n) one(i1);
-            }
+            const int o0 = off(lds16(ring + 2 * (h + (lane < n ? lane : 0))));
+            const int o1 = off(lds16(ring + 2 * (h + (lane + 32 < n ? lane + 32 : 0))));
+            const uint32_t v0 = h2_replace<ALE>(src, o0, a.k7);
+            const uint32_t v1 = h2_replace<ALE>(src, o1, a.k7);
+            if (lane < n) dst[o0] = static_cast<uint8_t>(v0);
+            if (lane + 32 < n) dst[o1] = static_cast<uint8_t>(v1);
         };
         if (ylo < yhi) {
             const uint8_t* colp = src + 16 + 8 * c;
