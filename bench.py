@@ -14,7 +14,8 @@ A step = one full k=5 denoise of this rank's batch (default workload c4:
   e2e       the same metric through the public host-buffer C ABI
             (phg_denoise_batch from pinned host memory: H2D, kernels, D2H of
             the images and per-iteration counters inside the timed region).
-  roofline  the dominant kernel (fused_tb_kernel, T=5 iterations per launch)
+  roofline  the dominant kernel (fused_h2_kernel for beta=1 / fused_tb_kernel for beta=2,
+            T iterations per launch)
             against MEASURED_PEAKS.json hbm_gbs, algorithmic bytes = 2 B per
             pixel-iteration.
   cpu_baseline  the reference's own CPU path (oracle/_ref, compiled from the
@@ -296,13 +297,14 @@ def kernel_roofline(R, src, dst, counters, params, w, h, n, beta, reps, row_base
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            tj = json.load(open(tpath))
-            traffic = tj.get(R.a.workload, {}).get("dram_bytes_per_launch")
+            tj = json.load(open(tpath)).get(R.a.workload, {})
+            if tj.get("kernel") == L.phg_fused_kernel_name(C.byref(params), T).decode():
+                traffic = tj.get("dram_bytes_per_launch")
         except Exception:
             pass
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
-            "kernel": f"fused_tb_kernel<beta={beta},T={T}>", "kernel_ms": round(k_ms, 4),
+            "kernel": L.phg_fused_kernel_name(C.byref(params), T).decode(), "kernel_ms": round(k_ms, 4),
             "alg_bytes_per_launch": int(alg_bytes)}
 
 

@@ -130,6 +130,10 @@ typedef struct phg_dev_image {
  * (temporal blocking depth; 0 if beta has no fused kernel). */
 int phg_max_fused_iterations(int beta);
 
+/* Name of the kernel one fused launch of `iters` iterations runs for these
+ * parameters (static string; "" if none).  For reports and profiles. */
+const char* phg_fused_kernel_name(const phg_params* p, int iters);
+
 /* One temporally blocked launch: `iters` (1..phg_max_fused_iterations)
  * fused cardinality+removal iterations, reading `src` and writing `dst`
  * (same geometry).  Buffer row y is global image row y + row_base of an

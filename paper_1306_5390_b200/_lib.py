@@ -23,6 +23,7 @@ EXPORTS = (
     "phg_denoise_pass", "phg_denoise", "phg_denoise_batch", "phg_synth_image",
     "phg_inject_sp_noise", "phg_max_fused_iterations", "phg_dev_fused_step",
     "phg_dev_denoise", "phg_dev_cardinality", "phg_dev_removal", "phg_finalize_stats",
+    "phg_fused_kernel_name",
 )
 
 
@@ -94,6 +95,8 @@ def lib():
         L.phg_finalize_stats.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(PhgPassStats),
                                          C.POINTER(C.c_int)]
         L.phg_max_fused_iterations.argtypes = [C.c_int]
+        L.phg_fused_kernel_name.argtypes = [C.POINTER(PhgParams), C.c_int]
+        L.phg_fused_kernel_name.restype = C.c_char_p
         _LIB = L
     return _LIB
 

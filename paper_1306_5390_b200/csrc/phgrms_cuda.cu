@@ -637,6 +637,21 @@ int phg_set_device(int device) {
 
 int phg_max_fused_iterations(int beta) { return max_fused(beta); }
 
+const char* phg_fused_kernel_name(const phg_params* p, int iters) {
+    static const char* const h2[] = {"", "fused_h2_kernel<T=1>", "fused_h2_kernel<T=2>", "fused_h2_kernel<T=3>",
+                                     "fused_h2_kernel<T=4>", "fused_h2_kernel<T=5>"};
+    static const char* const b1[] = {"", "fused_tb_kernel<beta=1,T=1>", "fused_tb_kernel<beta=1,T=2>",
+                                     "fused_tb_kernel<beta=1,T=3>", "fused_tb_kernel<beta=1,T=4>",
+                                     "fused_tb_kernel<beta=1,T=5>"};
+    static const char* const b2[] = {"", "fused_tb_kernel<beta=2,T=1>", "fused_tb_kernel<beta=2,T=2>",
+                                     "fused_tb_kernel<beta=2,T=3>", "fused_tb_kernel<beta=2,T=4>"};
+    if (!p || iters < 1) return "";
+    if (max_fused(p->beta) == 0) return iters == 1 ? "scalar_kernel<fused>" : "";
+    if (iters > max_fused(p->beta)) return "";
+    if (use_h2(*p, iters)) return h2[iters];
+    return p->beta == 1 ? b1[iters] : b2[iters];
+}
+
 int phg_finalize_stats(const uint64_t* ctr, int n, int kcap, phg_pass_stats* stats, int* iterations_run) {
     if (!ctr || !stats || !iterations_run || n < 0 || kcap < 1) return fail(PHG_EINVAL, "bad arguments");
     for (int i = 0; i < n; ++i) {
