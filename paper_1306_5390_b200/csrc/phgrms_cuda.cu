@@ -174,6 +174,35 @@ Launch plan_rows(int own_rows, int halo, int rows_target) {
     return {th, (own_rows + th - 1) / th};
 }
 
+// Output rows per tile for the two-tile kernel, wave-aware: the launch runs
+// ceil(CTAs / resident CTAs) waves of near-equal CTAs, each sweeping
+// T*sh - T(T+1) rows, so small grids (one 4K image = 240 CTAs of 36 rows on
+// 296 slots) pick the tile height that minimises waves x rows per CTA.
+Launch plan_rows_h2(int own_rows, int halo, int rows_target, int n_images, int tiles_x) {
+    static const int slots = [] {
+        int dev = 0, sms = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        return 2 * sms;  // two CTAs per SM (smem bound)
+    }();
+    const int th_max = std::max(1, rows_target - 2 * halo);
+    Launch best = plan_rows(own_rows, halo, rows_target);
+    double best_cost = 1e300;
+    for (int th = std::min(th_max, own_rows); th >= std::max(1, std::min(16, own_rows)); --th) {
+        const int64_t tiles_y = (own_rows + th - 1) / th;
+        const int64_t ctas = (static_cast<int64_t>(n_images) * tiles_x * tiles_y + 1) / 2;
+        const int64_t waves = (ctas + slots - 1) / slots;
+        const int sh = th + 2 * halo;
+        const double cost = static_cast<double>(waves) * (halo * sh - halo * (halo + 1) + 8);
+        if (cost < best_cost * 0.999) {
+            best_cost = cost;
+            best = {th, static_cast<int>(tiles_y)};
+        }
+    }
+    // even out the row tiles at the chosen count
+    const int th = (own_rows + best.tiles_y - 1) / best.tiles_y;
+    return {th, (own_rows + th - 1) / th};
+}
+
 using H2Fn = void (*)(const CUtensorMap, const phg::H2Args);
 
 template <int T, bool A>
@@ -194,7 +223,7 @@ H2Fn select_h2(int T, bool ale) {
 int h2_rows_target() {
     static const int v = [] {
         const char* e = getenv("PHG_H2_ROWS");
-        return e ? std::max(16, std::min(62, atoi(e))) : 46;
+        return e ? std::max(8, std::min(62, atoi(e))) : 46;
     }();
     return v;
 }
@@ -223,7 +252,8 @@ int launch_h2(const phg_dev_image& src, const phg_dev_image& dst, int row_base, 
     H2Fn fn = select_h2(iters, p.alpha <= 128);
     if (!fn) return fail(PHG_EINVAL, "no two-tile kernel for this iteration count");
     const int halo = iters;
-    const Launch L = plan_rows(own_hi - own_lo, halo, h2_rows_target());
+    const Launch L = plan_rows_h2(own_hi - own_lo, halo, h2_rows_target(), src.n_images,
+                                  (src.width + phg::kOutPx - 1) / phg::kOutPx);
     const int sh = L.th + 2 * halo;
     if (sh > phg::kH2MaxRows) return fail(PHG_EINVAL, "tile too tall");
     const size_t smem = phg::h2_smem_bytes(sh);
@@ -822,7 +852,11 @@ int phg_denoise_batch(const uint8_t* imgs, int n, int w, int h, const phg_params
     // Chunked pipeline over three streams: contiguous H2D of chunk i+1 and
     // D2H of chunk i-1 overlap the kernels of chunk i (host buffers should
     // be pinned for the copies to be asynchronous).
-    const int nchunks = std::min(n, n >= 64 ? 8 : 1);
+    static const int chunks_env = [] {
+        const char* e = getenv("PHG_BATCH_CHUNKS");
+        return e ? std::max(1, std::min(256, atoi(e))) : 8;
+    }();
+    const int nchunks = std::min(n, n >= 64 ? chunks_env : 1);
     const int per = (n + nchunks - 1) / nchunks;
     const int64_t pitch = round_up(w, 16);
     const int64_t img_bytes = static_cast<int64_t>(w) * h, img_pitched = pitch * h;
