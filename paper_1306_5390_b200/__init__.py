@@ -21,6 +21,7 @@ from .phgrms import (  # noqa: F401
     denoise_batch,
     denoise_pass,
     inject_sp_noise,
+    kernel_name,
     parallel_for_rows,
     residual_noise_count,
     rms_replacement,

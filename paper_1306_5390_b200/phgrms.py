@@ -303,3 +303,9 @@ def residual_noise_count(img: GrayImage, alpha: int, beta: int, card_threshold: 
     """metrics.hpp:52-59 -- pixels whose cardinality is below the threshold."""
     card = compute_cardinality(img, alpha, beta)
     return int(np.count_nonzero(card.counts < card_threshold))
+
+
+def kernel_name(params: DenoiseParams, iters: int) -> str:
+    """Which sm_100a kernel a fused launch of `iters` iterations runs for
+    these parameters (phg_fused_kernel_name)."""
+    return lib().phg_fused_kernel_name(C.byref(params._c()), int(iters)).decode()
