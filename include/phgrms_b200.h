@@ -162,6 +162,22 @@ int phg_dev_removal(const phg_dev_image* src, const int32_t* card, int64_t card_
                     const phg_params* p, const phg_dev_image* dst, uint64_t* counters,
                     void* stream);
 
+/* Metrics on either side of the denoise loop (metrics.hpp).
+ * residual_noise_count (metrics.hpp:52-59): pixels whose cardinality C is
+ * below card_threshold; beta = 1 runs the fp16 two-tile sweep without
+ * writing the map.  sse: the exact uint64 numerator of mse
+ * (metrics.hpp:25-35); mse = sse / (w*h), psnr from mse on the host.
+ * Errors: "alpha must be in [1, 255]", "beta must be >= 1",
+ * "card_threshold must be >= 1" (PHG_EINVAL). */
+int phg_residual_noise_count(const uint8_t* img, int width, int height, int alpha, int beta,
+                             int card_threshold, uint64_t* count);
+int phg_sse(const uint8_t* a, const uint8_t* b, int width, int height, uint64_t* sse);
+/* Device forms: counts[n_images] / sse[1] are device uint64 accumulated into
+ * (zero them first); a and b share geometry. */
+int phg_dev_residual_count(const phg_dev_image* img, int alpha, int beta, int card_threshold,
+                           uint64_t* counts, void* stream);
+int phg_dev_sse(const phg_dev_image* a, const phg_dev_image* b, uint64_t* sse, void* stream);
+
 /* Turn device counters into reference PassStats: per image, truncate after
  * the first iteration with replaced == 0 (denoise.hpp:308). */
 int phg_finalize_stats(const uint64_t* host_counters, int n_images, int kcap,

@@ -11,21 +11,27 @@ from .phgrms import (  # noqa: F401
     DenoiseResult,
     EngineMode,
     EngineSpec,
+    PsnrValue,
     GrayImage,
     NoiseSpec,
     PassStats,
     RowBlock,
     SynthKind,
+    cardmap,
     compute_cardinality,
     denoise,
     denoise_batch,
     denoise_pass,
     inject_sp_noise,
+    format_db,
     kernel_name,
+    mse,
+    psnr,
     parallel_for_rows,
     residual_noise_count,
     rms_replacement,
     row_blocks,
     similar,
     synth_image,
+    write_p2,
 )

@@ -23,7 +23,7 @@ EXPORTS = (
     "phg_denoise_pass", "phg_denoise", "phg_denoise_batch", "phg_synth_image",
     "phg_inject_sp_noise", "phg_max_fused_iterations", "phg_dev_fused_step",
     "phg_dev_denoise", "phg_dev_cardinality", "phg_dev_removal", "phg_finalize_stats",
-    "phg_fused_kernel_name",
+    "phg_fused_kernel_name", "phg_residual_noise_count", "phg_sse", "phg_dev_residual_count", "phg_dev_sse",
 )
 
 
@@ -97,6 +97,12 @@ def lib():
         L.phg_max_fused_iterations.argtypes = [C.c_int]
         L.phg_fused_kernel_name.argtypes = [C.POINTER(PhgParams), C.c_int]
         L.phg_fused_kernel_name.restype = C.c_char_p
+        L.phg_residual_noise_count.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                               C.POINTER(C.c_uint64)]
+        L.phg_sse.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_uint64)]
+        L.phg_dev_residual_count.argtypes = [C.POINTER(PhgDevImage), C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                             C.c_void_p]
+        L.phg_dev_sse.argtypes = [C.POINTER(PhgDevImage), C.POINTER(PhgDevImage), C.c_void_p, C.c_void_p]
         _LIB = L
     return _LIB
 

@@ -23,6 +23,7 @@
 
 #include "../../include/phgrms_b200.h"
 #include "kernel_b1.cuh"
+#include "kernel_card.cuh"
 #include "kernel_h2.cuh"
 #include "kernels.cuh"
 
@@ -286,6 +287,48 @@ int launch_h2(const phg_dev_image& src, const phg_dev_image& dst, int row_base, 
     a.counters = reinterpret_cast<unsigned long long*>(counters);
     const unsigned grid = static_cast<unsigned>((n_tiles + 1) / 2);
     fn<<<grid, phg::kH2Threads, smem, stream>>>(map, a);
+    ++g_launches;
+    PHG_CUDA(cudaGetLastError());
+    return PHG_OK;
+}
+
+// beta = 1 cardinality map (kCardMap) or C < thr count (kCardCount) over
+// whole images (rows = src.rows), fp16 two-tile sweep (kernel_card.cuh).
+int launch_card_h2(const phg_dev_image& src, int alpha, int mode, int thr, int32_t* card, int64_t card_pitch,
+                   uint64_t* counts, cudaStream_t stream) {
+    const Launch L = plan_rows_h2(src.rows, 1, 42, src.n_images, (src.width + phg::kOutPx - 1) / phg::kOutPx);
+    const int sh = L.th + 2;
+    const size_t smem = phg::card_smem_bytes(sh);
+    CUtensorMap map;
+    PHG_TRY(encode_map(&map, src, sh));
+    const void* fn = mode == phg::kCardMap ? reinterpret_cast<const void*>(phg::card_h2_kernel<phg::kCardMap>)
+                                           : reinterpret_cast<const void*>(phg::card_h2_kernel<phg::kCardCount>);
+    PHG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    phg::CardArgs a;
+    a.card = card;
+    a.card_pitch = card_pitch;
+    a.card_stride = card_pitch * src.rows;
+    a.width = src.width;
+    a.height = src.rows;
+    a.row_base = 0;
+    a.own_lo = 0;
+    a.own_hi = src.rows;
+    a.th = L.th;
+    a.tiles_x = (src.width + phg::kOutPx - 1) / phg::kOutPx;
+    a.tiles_y = L.tiles_y;
+    const int64_t n_tiles = static_cast<int64_t>(src.n_images) * a.tiles_x * a.tiles_y;
+    if (n_tiles > (int64_t(1) << 31) - 2) return fail(PHG_EINVAL, "too many tiles for one launch");
+    a.n_tiles = static_cast<int>(n_tiles);
+    const uint32_t ah = half_bits(static_cast<float>(alpha));
+    a.alpha2 = ah | (ah << 16);
+    const uint32_t th = half_bits(static_cast<float>(std::min(thr, 1025) - 1));
+    a.thr_h2 = th | (th << 16);
+    a.counts = reinterpret_cast<unsigned long long*>(counts);
+    const unsigned grid = static_cast<unsigned>((n_tiles + 1) / 2);
+    if (mode == phg::kCardMap)
+        phg::card_h2_kernel<phg::kCardMap><<<grid, 256, smem, stream>>>(map, a);
+    else
+        phg::card_h2_kernel<phg::kCardCount><<<grid, 256, smem, stream>>>(map, a);
     ++g_launches;
     PHG_CUDA(cudaGetLastError());
     return PHG_OK;
@@ -740,8 +783,54 @@ int phg_dev_cardinality(const phg_dev_image* src, int alpha, int beta, int32_t* 
     phg_params p{alpha, beta, 1, 1, 0};
     if (alpha < 1 || alpha > 255) return fail(PHG_EINVAL, "alpha must be in [1, 255]");
     if (beta < 1) return fail(PHG_EINVAL, "beta must be >= 1");
+    if (beta == 1 && !getenv("PHG_NO_H2"))
+        return launch_card_h2(*src, alpha, phg::kCardMap, 1, card, card_pitch, nullptr,
+                              static_cast<cudaStream_t>(stream));
     return launch_scalar(phg::kModeCard, *src, nullptr, nullptr, card, card_pitch, 0, src->rows, 0,
                          src->rows, p, 0, nullptr, 1, static_cast<cudaStream_t>(stream));
+}
+
+int phg_dev_residual_count(const phg_dev_image* src, int alpha, int beta, int card_threshold, uint64_t* counts,
+                           void* stream) {
+    if (alpha < 1 || alpha > 255) return fail(PHG_EINVAL, "alpha must be in [1, 255]");
+    if (beta < 1) return fail(PHG_EINVAL, "beta must be >= 1");
+    if (card_threshold < 1) return fail(PHG_EINVAL, "card_threshold must be >= 1");
+    if (!src || !counts) return fail(PHG_EINVAL, "null argument");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (beta == 1 && !getenv("PHG_NO_H2"))
+        return launch_card_h2(*src, alpha, phg::kCardCount, card_threshold, nullptr, 0, counts, st);
+    // wider windows: scalar map into scratch, then count
+    DeviceState* s;
+    PHG_TRY(current_state(&s));
+    void* pc;
+    const int64_t cpitch = round_up(src->width, 4);
+    PHG_TRY(scratch(s, 5, sizeof(int32_t) * cpitch * src->rows * src->n_images, &pc));
+    PHG_TRY(phg_dev_cardinality(src, alpha, beta, static_cast<int32_t*>(pc), cpitch, stream));
+    dim3 grid(std::max(1, std::min(1184, static_cast<int>((static_cast<int64_t>(src->width) * src->rows + 255) / 256))),
+              src->n_images);
+    phg::count_lt_kernel<<<grid, 256, 0, st>>>(static_cast<int32_t*>(pc), cpitch, src->width, src->rows,
+                                               src->n_images, card_threshold,
+                                               reinterpret_cast<unsigned long long*>(counts));
+    ++g_launches;
+    PHG_CUDA(cudaGetLastError());
+    return PHG_OK;
+}
+
+int phg_dev_sse(const phg_dev_image* a, const phg_dev_image* b, uint64_t* sse, void* stream) {
+    if (!a || !b || !sse) return fail(PHG_EINVAL, "null argument");
+    if (a->width != b->width || a->rows != b->rows || a->n_images != b->n_images || a->pitch != b->pitch ||
+        a->image_stride != b->image_stride)
+        return fail(PHG_EINVAL, "mse: image dimensions differ");
+    if ((reinterpret_cast<uintptr_t>(a->data) | reinterpret_cast<uintptr_t>(b->data) | a->pitch | a->image_stride) & 15)
+        return fail(PHG_EINVAL, "device images must be 16-byte aligned with 16-byte pitches");
+    const int64_t chunks = static_cast<int64_t>(a->n_images) * a->rows * ((a->width + 15) / 16);
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(148 * 8, (chunks + 255) / 256)));
+    phg::sse_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        a->data, b->data, a->pitch, a->image_stride, a->width, a->rows, a->n_images,
+        reinterpret_cast<unsigned long long*>(sse));
+    ++g_launches;
+    PHG_CUDA(cudaGetLastError());
+    return PHG_OK;
 }
 
 int phg_dev_removal(const phg_dev_image* src, const int32_t* card, int64_t card_pitch, const phg_params* p,
@@ -767,6 +856,48 @@ int phg_cardinality(const uint8_t* img, int w, int h, int alpha, int beta, int32
     PHG_TRY(phg_dev_cardinality(&im, alpha, beta, static_cast<int32_t*>(pc), cpitch, s->stream));
     PHG_CUDA(cudaMemcpy2DAsync(counts, sizeof(int32_t) * w, pc, sizeof(int32_t) * cpitch,
                                sizeof(int32_t) * w, h, cudaMemcpyDeviceToHost, s->stream));
+    PHG_CUDA(cudaStreamSynchronize(s->stream));
+    return PHG_OK;
+}
+
+int phg_residual_noise_count(const uint8_t* img, int w, int h, int alpha, int beta, int card_threshold,
+                             uint64_t* count) {
+    if (alpha < 1 || alpha > 255) return fail(PHG_EINVAL, "alpha must be in [1, 255]");
+    if (beta < 1) return fail(PHG_EINVAL, "beta must be >= 1");
+    if (card_threshold < 1) return fail(PHG_EINVAL, "card_threshold must be >= 1");
+    if (!img || !count) return fail(PHG_EINVAL, "null argument");
+    PHG_TRY(check_dims(w, h));
+    DeviceState* s;
+    PHG_TRY(current_state(&s));
+    void *pi, *pk;
+    const phg_dev_image in = make_image(nullptr, w, h, 1);
+    PHG_TRY(scratch(s, 0, in.image_stride, &pi));
+    PHG_TRY(scratch(s, 4, sizeof(uint64_t), &pk));
+    phg_dev_image im = make_image(pi, w, h, 1);
+    PHG_TRY(upload(im, img, s->stream));
+    PHG_CUDA(cudaMemsetAsync(pk, 0, sizeof(uint64_t), s->stream));
+    PHG_TRY(phg_dev_residual_count(&im, alpha, beta, card_threshold, static_cast<uint64_t*>(pk), s->stream));
+    PHG_CUDA(cudaMemcpyAsync(count, pk, sizeof(uint64_t), cudaMemcpyDeviceToHost, s->stream));
+    PHG_CUDA(cudaStreamSynchronize(s->stream));
+    return PHG_OK;
+}
+
+int phg_sse(const uint8_t* a, const uint8_t* b, int w, int h, uint64_t* sse) {
+    if (!a || !b || !sse) return fail(PHG_EINVAL, "null argument");
+    PHG_TRY(check_dims(w, h));
+    DeviceState* s;
+    PHG_TRY(current_state(&s));
+    void *pa, *pb, *pk;
+    const phg_dev_image in = make_image(nullptr, w, h, 1);
+    PHG_TRY(scratch(s, 0, in.image_stride, &pa));
+    PHG_TRY(scratch(s, 1, in.image_stride, &pb));
+    PHG_TRY(scratch(s, 4, sizeof(uint64_t), &pk));
+    phg_dev_image ia = make_image(pa, w, h, 1), ib = make_image(pb, w, h, 1);
+    PHG_TRY(upload(ia, a, s->stream));
+    PHG_TRY(upload(ib, b, s->stream));
+    PHG_CUDA(cudaMemsetAsync(pk, 0, sizeof(uint64_t), s->stream));
+    PHG_TRY(phg_dev_sse(&ia, &ib, static_cast<uint64_t*>(pk), s->stream));
+    PHG_CUDA(cudaMemcpyAsync(sse, pk, sizeof(uint64_t), cudaMemcpyDeviceToHost, s->stream));
     PHG_CUDA(cudaStreamSynchronize(s->stream));
     return PHG_OK;
 }

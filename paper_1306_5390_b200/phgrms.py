@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import math
 import os
 import threading
 from dataclasses import dataclass, field
@@ -300,9 +301,62 @@ def denoise_batch(imgs: np.ndarray, params: DenoiseParams):
 
 
 def residual_noise_count(img: GrayImage, alpha: int, beta: int, card_threshold: int) -> int:
-    """metrics.hpp:52-59 -- pixels whose cardinality is below the threshold."""
+    """metrics.hpp:52-59 -- pixels whose cardinality is below the threshold
+    (beta = 1: counted by the fp16 two-tile sweep, no map is written)."""
+    n = C.c_uint64(0)
+    a = np.ascontiguousarray(img.pixels, dtype=np.uint8)
+    check(lib().phg_residual_noise_count(a.ctypes.data, img.width, img.height, int(alpha), int(beta),
+                                         int(card_threshold), C.byref(n)))
+    return int(n.value)
+
+
+@dataclass
+class PsnrValue:
+    """metrics.hpp:18-22 -- +inf when the images are identical."""
+    decibels: float = 0.0
+
+    def infinite(self) -> bool:
+        return math.isinf(self.decibels)
+
+
+def mse(a: GrayImage, b: GrayImage) -> float:
+    """metrics.hpp:25-35 -- exact uint64 sum of squared differences on the
+    device (sse_kernel), one final double division."""
+    if not a.same_shape(b):
+        raise InvalidArgument("mse: image dimensions differ")
+    s = C.c_uint64(0)
+    pa = np.ascontiguousarray(a.pixels, dtype=np.uint8)
+    pb = np.ascontiguousarray(b.pixels, dtype=np.uint8)
+    check(lib().phg_sse(pa.ctypes.data, pb.ctypes.data, a.width, a.height, C.byref(s)))
+    return float(s.value) / float(a.size())
+
+
+def psnr(a: GrayImage, b: GrayImage) -> PsnrValue:
+    """metrics.hpp:37-42"""
+    m = mse(a, b)
+    if m == 0.0:
+        return PsnrValue(math.inf)
+    return PsnrValue(10.0 * math.log10(255.0 * 255.0 / m))
+
+
+def format_db(v: PsnrValue) -> str:
+    """metrics.hpp:44-50 -- 3 decimals, "inf" for identical images."""
+    return "inf" if v.infinite() else "%.3f" % v.decibels
+
+
+def write_p2(width: int, height: int, values, maxval: int) -> str:
+    """pgm.hpp:123-136 -- the cardinality-map P2 writer of `phgrms cardmap`
+    (tools/phgrms_main.cpp:151-168)."""
+    v = np.asarray(values, dtype=np.int64).reshape(height, width)
+    rows = [" ".join(map(str, r)) for r in v.tolist()]
+    return "P2\n%d %d\n%d\n" % (width, height, maxval) + "".join(r + "\n" for r in rows)
+
+
+def cardmap(img: GrayImage, alpha: int = 20, beta: int = 1) -> str:
+    """`phgrms cardmap` (tools/phgrms_main.cpp:151-168): the P2 dump of
+    compute_cardinality with maxval = (2 beta + 1)^2."""
     card = compute_cardinality(img, alpha, beta)
-    return int(np.count_nonzero(card.counts < card_threshold))
+    return write_p2(card.width, card.height, card.counts, (2 * beta + 1) * (2 * beta + 1))
 
 
 def kernel_name(params: DenoiseParams, iters: int) -> str:

@@ -9,7 +9,9 @@
 
 #include "phgrms/denoise.hpp"
 #include "phgrms/image.hpp"
+#include "phgrms/metrics.hpp"
 #include "phgrms/noise.hpp"
+#include "phgrms/pgm.hpp"
 
 using namespace phgrms;
 
@@ -160,6 +162,45 @@ int main() {
     {  // noise fixture (test_noise.cpp:43-62) through the drop-in generator
         const auto [noisy, mask] = inject_sp_noise(GrayImage(10, 10, 100), {0.2, 0.5, 77});
         CHECK(noisy.pixels[4] == 255 && noisy.pixels[2] == 0 && mask.count() == 20);
+    }
+    {  // metrics.hpp: test_cli.cpp:76-95 fixture and acceptance.cpp:305-320
+        const GrayImage a(8, 8, 40);
+        GrayImage b = a;
+        for (auto& p : b.pixels) p += 16;
+        CHECK(mse(a, a) == 0.0 && psnr(a, a).infinite() && format_db(psnr(a, a)) == "inf");
+        CHECK(mse(a, b) == 256.0 && format_db(psnr(a, b)) == "24.048");
+        CHECK_THROWS_AS(mse(GrayImage(4, 4, 1), GrayImage(4, 5, 1)), std::invalid_argument);
+        CHECK(format_db(psnr(GrayImage(1, 1, 0), GrayImage(1, 1, 255))) == "0.000");
+        std::mt19937 rng(7);
+        const GrayImage x = random_image(rng, 333, 77), y = random_image(rng, 333, 77);
+        std::uint64_t s = 0;
+        for (std::size_t i = 0; i < x.size(); ++i) {
+            const int d = int(x.pixels[i]) - int(y.pixels[i]);
+            s += std::uint64_t(d * d);
+        }
+        CHECK(mse(x, y) == double(s) / double(x.size()));
+    }
+    {  // residual_noise_count == count of C < thr of compute_cardinality (metrics.hpp:52-59)
+        std::mt19937 rng(9);
+        for (int i = 0; i < 20; ++i) {
+            const GrayImage img = random_image(rng, 1 + static_cast<int>(rng() % 700), 1 + static_cast<int>(rng() % 60));
+            const int alpha = 1 + static_cast<int>(rng() % 80), beta = 1 + static_cast<int>(rng() % 3);
+            const int thr = 1 + static_cast<int>(rng() % 6);
+            const auto card = compute_cardinality(img, alpha, beta);
+            std::size_t n = 0;
+            for (auto c : card.counts) n += c < thr;
+            CHECK(residual_noise_count(img, alpha, beta, thr) == n);
+        }
+    }
+    {  // cardmap P2 text (test_cli.cpp:113-131)
+        const auto c1 = compute_cardinality(GrayImage(3, 3, 100), 20, 1);
+        CHECK(write_p2(c1.width, c1.height, c1.counts, 9) == "P2\n3 3\n9\n4 6 4\n6 9 6\n4 6 4\n");
+        GrayImage imp(3, 3, 100);
+        imp.at(1, 1) = 255;
+        const auto c2 = compute_cardinality(imp, 20, 1);
+        CHECK(write_p2(c2.width, c2.height, c2.counts, 9) == "P2\n3 3\n9\n3 5 3\n5 1 5\n3 5 3\n");
+        const auto c3 = compute_cardinality(GrayImage(3, 3, 100), 20, 2);
+        CHECK(write_p2(c3.width, c3.height, c3.counts, 25).substr(0, 9) == "P2\n3 3\n25");
     }
     std::printf("dropin: %d checks, %d failures\n", g_checks, g_fail);
     return g_fail ? 1 : 0;
