@@ -4,9 +4,15 @@
 // API, unchanged, now running on the B200 kernels.  Built by
 // __graft_entry__.build(); run by tests/test_dropin_gpu.py on a GPU.
 #include <cstdio>
+#include <fstream>
+#include <iterator>
+#include <limits>
+#include <sstream>
+#include <string>
 #include <random>
 #include <stdexcept>
 
+#include "phgrms/bench.hpp"
 #include "phgrms/denoise.hpp"
 #include "phgrms/image.hpp"
 #include "phgrms/metrics.hpp"
@@ -16,6 +22,7 @@
 using namespace phgrms;
 
 static int g_fail = 0, g_checks = 0;
+static std::string g_golden_dir = "tests/golden";
 #define CHECK(x)                                                              \
     do {                                                                      \
         ++g_checks;                                                           \
@@ -41,7 +48,8 @@ static GrayImage random_image(std::mt19937& rng, int w, int h) {
     return img;
 }
 
-int main() {
+int main(int argc, char** argv) {
+    if (argc > 1) g_golden_dir = argv[1];
     {  // cardinality of a constant image equals the in-bounds window size
         const auto card = compute_cardinality(GrayImage(3, 3, 100), 20, 1);
         CHECK((card.counts == std::vector<std::int32_t>{4, 6, 4, 6, 9, 6, 4, 6, 4}));
@@ -201,6 +209,114 @@ int main() {
         CHECK(write_p2(c2.width, c2.height, c2.counts, 9) == "P2\n3 3\n9\n3 5 3\n5 1 5\n3 5 3\n");
         const auto c3 = compute_cardinality(GrayImage(3, 3, 100), 20, 2);
         CHECK(write_p2(c3.width, c3.height, c3.counts, 25).substr(0, 9) == "P2\n3 3\n25");
+    }
+    {  // pgm.hpp codec (test_pgm.cpp)
+        const auto img = read_pgm("P2\n2 2\n255\n0 64 128 255");
+        CHECK(img.width == 2 && img.height == 2 && (img.pixels == std::vector<std::uint8_t>{0, 64, 128, 255}));
+        CHECK(write_pgm(GrayImage(1, 1, 200)) == std::string("P5\n1 1\n255\n") + '\xC8');
+        CHECK(write_pgm(GrayImage(2, 3, 9)).size() == std::string("P5\n2 3\n255\n").size() + 6);
+        std::mt19937 rng(7);
+        for (int i = 0; i < 25; ++i) {
+            const GrayImage r = random_image(rng, 1 + static_cast<int>(rng() % 20), 1 + static_cast<int>(rng() % 20));
+            CHECK(read_pgm(write_pgm(r, false)) == r && read_pgm(write_pgm(r, true)) == r);
+        }
+        CHECK((read_pgm("P2\n# produced by hand\n2 1 # dims\n# maxval next\n255\n3 4").pixels ==
+               std::vector<std::uint8_t>{3, 4}));
+        CHECK((read_pgm("P5\n# note\n1 1\n255\n" + std::string(1, '\x05')).pixels == std::vector<std::uint8_t>{5}));
+        CHECK((read_pgm("P2\n2 1\n15\n0 15").pixels == std::vector<std::uint8_t>{0, 15}));
+        auto msg = [](const std::string& s) {
+            try {
+                (void)read_pgm(s);
+            } catch (const PgmError& e) {
+                return std::string(e.what());
+            }
+            return std::string("no error");
+        };
+        CHECK(msg("P2\n2 1\n15\n0 16") == "PGM pixel value exceeds maxval");
+        CHECK(msg("P2\n1 1\n65535\n1234") == "16-bit PGM unsupported");
+        CHECK(msg(std::string("P5\n1 1\n256\n") + '\0') == "16-bit PGM unsupported");
+        CHECK(msg("P6\n1 1\n255\nxxx") == "not a PGM stream (expected P2 or P5 magic)");
+        CHECK(msg("") == "not a PGM stream (expected P2 or P5 magic)");
+        CHECK(msg("P2\n1\n255\n0") != "no error" && msg("P2\n0 1\n255\n") == "malformed PGM header");
+        CHECK(msg("P5\n2 2\n255\nab") == "truncated PGM pixel data");
+        CHECK(msg("P2\n2 2\n255\n1 2 3") == "truncated PGM pixel data");
+    }
+    {  // bench.hpp grid + CSV (test_bench.cpp)
+        const std::string hdr =
+            "image_id,width,height,noise_pct,engine,workers,iterations_run,"
+            "total_ms,psnr_noisy_db,psnr_denoised_db,replaced_total\n";
+        CHECK(write_csv({}) == hdr);
+        BenchRecord rec;
+        rec.image_id = "smooth-16";
+        rec.width = rec.height = 16;
+        rec.noise_pct = 5.0;
+        rec.engine = "serial";
+        rec.workers = 1;
+        rec.iterations_run = 2;
+        rec.total_ms = 1.2345;
+        rec.psnr_noisy_db = 18.7;
+        rec.psnr_denoised_db = std::numeric_limits<double>::infinity();
+        rec.replaced_total = 12;
+        CHECK(write_csv({rec}) == hdr + "smooth-16,16,16,5.000,serial,1,2,1.234,18.700,inf,12\n");
+        BenchConfig cfg;
+        cfg.synth_sizes = {24};
+        cfg.densities = {0.10};
+        cfg.repetitions = 1;
+        cfg.engines = {EngineSpec::serial(), EngineSpec::parallel(2), EngineSpec::parallel(3)};
+        const auto res = run_benchmark(cfg);
+        CHECK(res.records.size() == 3);
+        if (res.records.size() == 3) {
+            const auto& s0 = res.records[0];
+            CHECK(s0.engine == "serial" && s0.workers == 1 && s0.total_ms > 0.0);
+            CHECK(s0.iterations_run >= 1 && s0.iterations_run <= cfg.params.max_iterations);
+            for (const auto& r : res.records)
+                CHECK(r.psnr_denoised_db == s0.psnr_denoised_db && r.psnr_noisy_db == s0.psnr_noisy_db &&
+                      r.replaced_total == s0.replaced_total && r.total_ms > 0.0);
+        }
+        BenchConfig g2;
+        g2.synth_sizes = {8, 12};
+        g2.densities = {0.05, 0.20};
+        g2.repetitions = 1;
+        g2.engines = {EngineSpec::serial(), EngineSpec::parallel(2)};
+        const auto r2 = run_benchmark(g2);
+        CHECK(r2.records.size() == 8 && r2.warnings.empty());
+        BenchConfig g3;
+        g3.corpus_files = {"/nonexistent/missing.pgm"};
+        g3.synth_sizes = {8};
+        g3.densities = {0.1};
+        g3.repetitions = 1;
+        g3.engines = {EngineSpec::serial()};
+        const auto r3 = run_benchmark(g3);
+        CHECK(r3.warnings.size() == 1 && r3.warnings[0].find("missing.pgm") != std::string::npos &&
+              r3.records.size() == 1);
+        BenchConfig g4;
+        g4.synth_sizes = {};
+        CHECK_THROWS_AS(run_benchmark(g4), std::invalid_argument);
+        // the reference harness's own output for a 3 x 3 x 2 grid
+        // (tests/golden/bench_grid.csv, make_bench_golden.cpp): every column
+        // but the wall time must match
+        BenchConfig g5;
+        g5.synth_sizes = {24, 64, 200};
+        g5.densities = {0.05, 0.30, 0.70};
+        g5.engines = {EngineSpec::serial(), EngineSpec::parallel(3)};
+        g5.repetitions = 1;
+        g5.seed = 5;
+        auto r5 = run_benchmark(g5);
+        for (auto& r : r5.records) r.total_ms = 0.0;
+        std::string got;
+        {
+            std::istringstream in(write_csv(r5.records));
+            std::string line;
+            while (std::getline(in, line)) {
+                std::string out, cur;
+                std::istringstream ls(line);
+                for (int f = 0; std::getline(ls, cur, ','); ++f) out += (out.empty() ? "" : ",") + (f == 7 ? "-" : cur);
+                got += out + "\n";
+            }
+        }
+        std::ifstream gf(g_golden_dir + "/bench_grid.csv");
+        const std::string want((std::istreambuf_iterator<char>(gf)), std::istreambuf_iterator<char>());
+        CHECK(!want.empty() && got == want);
     }
     std::printf("dropin: %d checks, %d failures\n", g_checks, g_fail);
     return g_fail ? 1 : 0;

@@ -19,6 +19,6 @@ def test_dropin_headers_compile():
 def test_dropin_reference_tests_on_gpu():
     import __graft_entry__ as g
     g.build_dropin()
-    r = subprocess.run([BIN], capture_output=True, text=True, timeout=300)
+    r = subprocess.run([BIN, os.path.join(ROOT, "tests", "golden")], capture_output=True, text=True, timeout=300)
     print(r.stdout, r.stderr)
     assert r.returncode == 0 and "0 failures" in r.stdout
