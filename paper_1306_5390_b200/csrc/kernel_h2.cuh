@@ -230,7 +230,8 @@ __global__ void __launch_bounds__(kH2Threads, 2)
         if (hasB) tma_load_4d(smem + bufb + h2_stage_b(sh), &src_map, 0, x0B / kChunk, y0B, imgB, &bar);
     }
     if (tid < 4 * T) (&red[0][0])[tid] = 0;
-    // quad bit b = 8k + 4h + (3 - row in quad): column byte k + 4h (see the slot layout below)
+    // quad bit b = 8k + 4h + (3 - row in quad) -> byte offset from the quad's
+    // first row and the lane's column 0 (column byte k + 4h; slot layout below)
     if (tid < 32) otab[tid] = static_cast<uint16_t>((3 - (tid & 3)) * kH2RP + (tid >> 3) + (tid & 4));
 
     // ---- per-thread column constants (4 columns x 2 tiles = 8 slots)
@@ -325,12 +326,9 @@ __global__ void __launch_bounds__(kH2Threads, 2)
         // process ring[h, h+n), n <= 64: two independent candidates per lane
         auto drain = [&](int h, int n) {
             // item = quad << 10 | lane << 5 | bit (quad = first row / 4)
-            auto off = [&](uint32_t it) {
-                return static_cast<int>(it >> 10) * (4 * kH2RP) + c_w + 8 * static_cast<int>((it >> 5) & 31) +
-                       otab[it & 31];
-            };
-            const int o0 = off(lds16(ring + 2 * (h + (lane < n ? lane : 0))));
-            const int o1 = off(lds16(ring + 2 * (h + (lane + 32 < n ? lane + 32 : 0))));
+            // items are byte offsets of candidates in the interleaved tile
+            const int o0 = static_cast<int>(lds16(ring + 2 * (h + (lane < n ? lane : 0))));
+            const int o1 = static_cast<int>(lds16(ring + 2 * (h + (lane + 32 < n ? lane + 32 : 0))));
             const uint32_t v0 = h2_replace<ALE>(src, o0, a.k7);
             const uint32_t v1 = h2_replace<ALE>(src, o1, a.k7);
             if (lane < n) dst[o0] = static_cast<uint8_t>(v0);
@@ -368,13 +366,13 @@ __global__ void __launch_bounds__(kH2Threads, 2)
                 const int total = __shfl_sync(0xffffffffu, incl, 31);
                 if (total) {
                     uint32_t addr = ring + 2 * (pending + incl - n);
-                    const uint32_t base = (static_cast<uint32_t>(y0 >> 2) << 10) | (lane << 5);
+                    const uint32_t base = static_cast<uint32_t>(y0 * kH2RP + 16 + 8 * c);
                     uint32_t mm = R;
                     while (mm) {
                         uint32_t b;
                         asm("bfind.u32 %0, %1;" : "=r"(b) : "r"(mm));
                         mm ^= 1u << b;
-                        sts16(addr, base | b);
+                        sts16(addr, base + otab[b]);
                         addr += 2;
                     }
                     pending += total;
