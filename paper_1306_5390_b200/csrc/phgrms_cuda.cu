@@ -463,7 +463,11 @@ int step(const phg_dev_image& src, const phg_dev_image& dst, int row_base, int h
 
 // Split k iterations into launches of at most max_fused(beta), evenly.
 std::vector<int> chunk_plan(int k, int beta) {
-    const int tmax = std::max(1, max_fused(beta));
+    static const int cap = [] {
+        const char* e = getenv("PHG_TMAX");  // temporal-blocking depth cap (tuning)
+        return e ? std::max(1, atoi(e)) : 1 << 20;
+    }();
+    const int tmax = std::max(1, std::min(cap, max_fused(beta)));
     const int n = (k + tmax - 1) / tmax;
     std::vector<int> c(n, k / n);
     for (int i = 0; i < k % n; ++i) ++c[i];
