@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(256, 2) card_h2_kernel(const __grid_constant__
     const int ylo = HALO + g * rows / 2, yhi = HALO + (g + 1) * rows / 2;
     uint32_t flh = 0;
     if (ylo < yhi) {
-        const uint8_t* colp = smem + 16 + 8 * c;
+        const uint32_t colp = smem_u32(smem) + 16 + 8 * c;
         auto row_oob = [&](int y) {
             const int ra = gyA + y, rb = gyB + y;
             return ((ra >= 0 && ra < H) ? 0u : 0x00100010u) | ((!hasB || (rb >= 0 && rb < H)) ? 0u : 0x10001000u);

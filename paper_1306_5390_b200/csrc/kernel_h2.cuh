@@ -109,12 +109,32 @@ __device__ __forceinline__ uint32_t f2h(float f) {
 }
 __device__ __forceinline__ uint32_t h2pack(float lo, float hi) { return f2h(lo) | (f2h(hi) << 16); }
 
+// Shared-memory accesses by 32-bit shared address (no generic-address
+// arithmetic in the row loop).  The "memory" clobber keeps them ordered with
+// the barriers and the stores.
+__device__ __forceinline__ uint32_t lds32a(uint32_t a) {
+    uint32_t v;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint2 lds64a(uint32_t a) {
+    uint2 v;
+    asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts64a(uint32_t a, uint2 v) {
+    asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(v.x), "r"(v.y) : "memory");
+}
+__device__ __forceinline__ void sts8a(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
 // The per-thread view of one staged row: 6 half2 = columns x-1 .. x+4, lane 0
 // tile A, lane 1 tile B.  kc[] holds the exponent bytes per column.
-__device__ __forceinline__ void h2_load_row(const uint8_t* rowp, const uint32_t (&kc)[4], uint32_t row_oob,
+__device__ __forceinline__ void h2_load_row(uint32_t rowa, const uint32_t (&kc)[4], uint32_t row_oob,
                                             uint32_t (&v)[6], uint2& raw) {
-    raw = *reinterpret_cast<const uint2*>(rowp);
-    const uint32_t wl = lds32(rowp - 4), wr = lds32(rowp + 8);
+    raw = lds64a(rowa);
+    const uint32_t wl = lds32a(rowa - 4), wr = lds32a(rowa + 8);
     v[0] = prmt(wl, kc[0] | row_oob, 0x7362);
     v[1] = prmt(raw.x, kc[1] | row_oob, 0x5140);
     v[2] = prmt(raw.x, kc[1] | row_oob, 0x7362);
@@ -163,7 +183,7 @@ __device__ __forceinline__ uint32_t lds16(uint32_t addr) {
 // `o` = byte offset of the pixel in the interleaved tile; returns the new
 // value (no store, so that two candidates' loads can be interleaved).
 template <bool ALE>
-__device__ __forceinline__ uint32_t h2_replace(const uint8_t* src, int o, uint32_t k7) {
+__device__ __forceinline__ uint32_t h2_replace(uint32_t src, int o, uint32_t k7) {
     const int o1 = o - kH2RP - 2;
     const int b4 = o1 & ~3;
     const uint32_t sh = static_cast<uint32_t>(o1 & 3);
@@ -171,8 +191,8 @@ __device__ __forceinline__ uint32_t h2_replace(const uint8_t* src, int o, uint32
     uint32_t R[3];
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
-        const uint8_t* p = src + b4 + r * kH2RP;
-        R[r] = prmt(lds32(p), lds32(p + 4), sel);
+        const uint32_t p = src + b4 + r * kH2RP;
+        R[r] = prmt(lds32a(p), lds32a(p + 4), sel);
     }
     const uint32_t n1 = prmt(R[0], R[1], 0x4210);  // t0 t1 t2 m0
     const uint32_t n2 = prmt(R[1], R[2], 0x6542);  // m2 b0 b1 b2
@@ -308,8 +328,8 @@ __global__ void __launch_bounds__(kH2Threads, 2)
     const int c_w = 16 + 8 * (c - lane);  // interleaved byte offset of lane 0's column 0
 
     for (int t = 0; t < T; ++t) {
-        const uint8_t* src = smem + ((t & 1) ? bufb : 0);
-        uint8_t* dst = smem + ((t & 1) ? 0 : bufb);
+        const uint32_t src = smem_u32(smem) + ((t & 1) ? bufb : 0);
+        const uint32_t dst = smem_u32(smem) + ((t & 1) ? 0 : bufb);
         const int ylo = max(g_lo, t + 1);
         const int yhi = min(g_hi, sh - 1 - t);
         // per-byte nibble counters of own candidate bits (flushed every 15 rows)
@@ -331,11 +351,11 @@ __global__ void __launch_bounds__(kH2Threads, 2)
             const int o1 = static_cast<int>(lds16(ring + 2 * (h + (lane + 32 < n ? lane + 32 : 0))));
             const uint32_t v0 = h2_replace<ALE>(src, o0, a.k7);
             const uint32_t v1 = h2_replace<ALE>(src, o1, a.k7);
-            if (lane < n) dst[o0] = static_cast<uint8_t>(v0);
-            if (lane + 32 < n) dst[o1] = static_cast<uint8_t>(v1);
+            if (lane < n) sts8a(dst + o0, v0);
+            if (lane + 32 < n) sts8a(dst + o1, v1);
         };
         if (ylo < yhi) {
-            const uint8_t* colp = src + 16 + 8 * c;
+            const uint32_t colp = src + 16 + 8 * c;
             auto row_oob = [&](int y) {
                 const int ra = gyA + y, rb = gyB + y;
                 return ((ra >= 0 && ra < H) ? 0u : 0x00100010u) | ((!hasB || (rb >= 0 && rb < H)) ? 0u : 0x10001000u);
@@ -410,7 +430,7 @@ __global__ void __launch_bounds__(kH2Threads, 2)
                 }
                 // the centre row goes to the destination unchanged (candidates are
                 // overwritten by the replacement pass)
-                *reinterpret_cast<uint2*>(dst + y * kH2RP + 16 + 8 * c) = raw;
+                sts64a(dst + y * kH2RP + 16 + 8 * c, raw);
                 // row classes (warp-uniform)
                 uint32_t intm = colint;
                 uint32_t ownm;
