@@ -372,10 +372,14 @@ __global__ void __launch_bounds__(kH2Threads, 2)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) up[j] = h2add(h2add(s[j], d[j]), aa[j + 1]);
             }
-            int nrow = 0;
+            // owned-pixel mask, recomputed only where it changes (rows HALO,
+            // HALO + outA, HALO + outB; warp-uniform)
+            uint32_t ownm = 0;
+            int next_own = ylo;
             uint32_t R = 0;  // candidate bits of the current row quad (rows y0 .. y0+3, y0 % 4 == 0)
             // append the quad's interior candidates to the warp ring; drain full rounds
             auto push = [&](int y0) {
+                if (y0 & 4) flush();  // every 8 rows: the nibble counters never exceed 8
                 const int n = __popc(R);
                 int incl = n;
 #pragma unroll
@@ -433,11 +437,15 @@ __global__ void __launch_bounds__(kH2Threads, 2)
                 sts64a(dst + y * kH2RP + 16 + 8 * c, raw);
                 // row classes (warp-uniform)
                 uint32_t intm = colint;
-                uint32_t ownm;
-                {
+                if (y == next_own) {
                     const uint32_t oa = (y >= HALO && y < HALO + outA) ? 0x00ff00ffu : 0u;
                     const uint32_t ob = (y >= HALO && y < HALO + outB) ? 0xff00ff00u : 0u;
                     ownm = colown & (oa | ob);
+                    int nx = 1 << 30;
+                    if (HALO > y) nx = min(nx, HALO);
+                    if (HALO + outA > y) nx = min(nx, HALO + outA);
+                    if (HALO + outB > y) nx = min(nx, HALO + outB);
+                    next_own = nx;
                 }
                 uint32_t vn[4];
                 if (FAST) {
@@ -463,10 +471,6 @@ __global__ void __launch_bounds__(kH2Threads, 2)
                 const uint32_t Mi = M & intm;
                 fl_n += M & ownm;
                 rp_n += Mi & ownm;
-                if (++nrow == 15) {
-                    flush();
-                    nrow = 0;
-                }
                 R = (R << 1) | Mi;
                 if ((y & 3) == 3) push(y - 3);
 #pragma unroll
