@@ -86,3 +86,17 @@ def test_flat_image_stops_early_through_h2():
     assert [s.replaced for s in res.stats] == [1526, 25, 0]
     ref_img, _ = O.denoise(noisy)
     assert np.array_equal(res.image.pixels, ref_img)
+
+
+@pytest.mark.parametrize("beta,k,border", [(1, 5, 0), (1, 12, 0), (2, 5, 0), (2, 9, 1), (3, 2, 0)])
+def test_row_pipelined_single_image(beta, k, border):
+    # images >= 32 MB go host -> device -> host in row chunks (denoise_rows_pipelined)
+    clean = O.synth_image(4096, 8193, 31 + beta)
+    noisy = O.inject_sp_noise(clean, 0.4, 0.5, 7 + k)
+    res = P.denoise(P.GrayImage.from_array(noisy), P.DenoiseParams(20, beta, k, 3, P.BorderMode(border)))
+    ref_img, ref_stats = O.denoise(noisy, 20, beta, k, 3, border)
+    assert np.array_equal(res.image.pixels, ref_img)
+    assert [(s.flagged, s.replaced) for s in res.stats] == ref_stats
+    out, stats = P.denoise_batch(noisy[None], P.DenoiseParams(20, beta, k, 3, P.BorderMode(border)))
+    assert np.array_equal(out[0], ref_img)
+    assert [(s.flagged, s.replaced) for s in stats[0]] == ref_stats
