@@ -50,7 +50,8 @@ constexpr int kH2MaxRows = 62;            // ring items are u16 byte offsets: sh
 // the two [sh][528] tiles (B at a 128-byte aligned offset)
 __host__ __device__ constexpr int h2_stage_b(int sh) { return (kRP * sh + 127) / 128 * 128; }
 __host__ __device__ constexpr int h2_buf_bytes(int sh) { return (kH2RP * sh + 128 + 127) / 128 * 128; }
-constexpr int kH2Ring = 64 + 32 * 32;  // per-warp u16 items: < 64 leftovers + one row quad
+constexpr int kH2Round = 96;           // drained per round: three candidates per lane
+constexpr int kH2Ring = kH2Round + 32 * 32;  // per-warp u16 items: leftovers + one row quad
 __host__ __device__ constexpr int h2_smem_bytes(int sh) {
     return 2 * h2_buf_bytes(sh) + (kH2Threads / 32) * kH2Ring * 2;
 }
@@ -349,10 +350,13 @@ __global__ void __launch_bounds__(kH2Threads, 2)
             // items are byte offsets of candidates in the interleaved tile
             const int o0 = static_cast<int>(lds16(ring + 2 * (h + (lane < n ? lane : 0))));
             const int o1 = static_cast<int>(lds16(ring + 2 * (h + (lane + 32 < n ? lane + 32 : 0))));
+            const int o2 = static_cast<int>(lds16(ring + 2 * (h + (lane + 64 < n ? lane + 64 : 0))));
             const uint32_t v0 = h2_replace<ALE>(src, o0, a.k7);
             const uint32_t v1 = h2_replace<ALE>(src, o1, a.k7);
+            const uint32_t v2 = h2_replace<ALE>(src, o2, a.k7);
             if (lane < n) sts8a(dst + o0, v0);
             if (lane + 32 < n) sts8a(dst + o1, v1);
+            if (lane + 64 < n) sts8a(dst + o2, v2);
         };
         if (ylo < yhi) {
             const uint32_t colp = src + 16 + 8 * c;
@@ -401,17 +405,19 @@ __global__ void __launch_bounds__(kH2Threads, 2)
                     }
                     pending += total;
                     __syncwarp();
-                    if (pending >= 64) {
+                    if (pending >= kH2Round) {
                         int h = 0;
-                        for (; pending - h >= 64; h += 64) drain(h, 64);
+                        for (; pending - h >= kH2Round; h += kH2Round) drain(h, kH2Round);
                         pending -= h;
                         __syncwarp();
-                        if (pending) {  // move the < 64 leftovers to the front
+                        if (pending) {  // move the leftovers (< kH2Round) to the front
                             const uint32_t l0 = lane < pending ? lds16(ring + 2 * (h + lane)) : 0;
                             const uint32_t l1 = lane + 32 < pending ? lds16(ring + 2 * (h + lane + 32)) : 0;
+                            const uint32_t l2 = lane + 64 < pending ? lds16(ring + 2 * (h + lane + 64)) : 0;
                             __syncwarp();
                             if (lane < pending) sts16(ring + 2 * lane, l0);
                             if (lane + 32 < pending) sts16(ring + 2 * (lane + 32), l1);
+                            if (lane + 64 < pending) sts16(ring + 2 * (lane + 64), l2);
                         }
                         __syncwarp();
                     }
