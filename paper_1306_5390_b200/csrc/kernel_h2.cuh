@@ -216,7 +216,6 @@ __global__ void __launch_bounds__(kH2Threads, 2)
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint64_t bar;
     __shared__ unsigned int red[T][4];  // flagged A, flagged B, replaced A, replaced B
-    __shared__ uint16_t otab[32];       // byte offset of candidate bit b relative to its quad
 
     const int sh = a.th + 2 * HALO;
     const int bufb = h2_buf_bytes(sh);
@@ -251,9 +250,6 @@ __global__ void __launch_bounds__(kH2Threads, 2)
         if (hasB) tma_load_4d(smem + bufb + h2_stage_b(sh), &src_map, 0, x0B / kChunk, y0B, imgB, &bar);
     }
     if (tid < 4 * T) (&red[0][0])[tid] = 0;
-    // quad bit b = 8k + 4h + (3 - row in quad) -> byte offset from the quad's
-    // first row and the lane's column 0 (column byte k + 4h; slot layout below)
-    if (tid < 32) otab[tid] = static_cast<uint16_t>((3 - (tid & 3)) * kH2RP + (tid >> 3) + (tid & 4));
 
     // ---- per-thread column constants (4 columns x 2 tiles = 8 slots)
     const int c = tid % kH2Cols;
@@ -394,13 +390,14 @@ __global__ void __launch_bounds__(kH2Threads, 2)
                 const int total = __shfl_sync(0xffffffffu, incl, 31);
                 if (total) {
                     uint32_t addr = ring + 2 * (pending + incl - n);
-                    const uint32_t base = static_cast<uint32_t>(y0 * kH2RP + 16 + 8 * c);
+                    // bit b = 8k + 4h + s: row y0 + 3 - s, column byte k + 4h
+                    const uint32_t base3 = static_cast<uint32_t>((y0 + 3) * kH2RP + 16 + 8 * c);
                     uint32_t mm = R;
                     while (mm) {
                         uint32_t b;
                         asm("bfind.u32 %0, %1;" : "=r"(b) : "r"(mm));
                         mm ^= 1u << b;
-                        sts16(addr, base + otab[b]);
+                        sts16(addr, base3 - (b & 3u) * kH2RP + (b >> 3) + (b & 4u));
                         addr += 2;
                     }
                     pending += total;
