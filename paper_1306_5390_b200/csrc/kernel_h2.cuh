@@ -322,7 +322,6 @@ __global__ void __launch_bounds__(kH2Threads, 2)
     const int f_hi = min(H - 1 - gyA, hasB ? H - 1 - gyB : 1000000);  // exclusive
     const int g_lo = g == 0 ? 1 : sh / 2;
     const int g_hi = g == 0 ? sh / 2 : sh - 1;
-    const int c_w = 16 + 8 * (c - lane);  // interleaved byte offset of lane 0's column 0
 
     for (int t = 0; t < T; ++t) {
         const uint32_t src = smem_u32(smem) + ((t & 1) ? bufb : 0);

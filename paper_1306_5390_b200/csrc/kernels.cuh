@@ -456,7 +456,9 @@ __global__ void __launch_bounds__(kThreads)
         const int yint_lo = min(max(ylo, BETA - gy0), yhi);
         const int yint_hi = max(min(yhi, a.height - BETA - gy0), yint_lo);
         uint32_t fl_acc = 0, rp_acc = 0;  // per-lane counts (bytes; < 256 rows per thread)
-        uint32_t cb0 = 0, cb1 = 0, cb2 = 0, cb3 = 0;  // candidate shift register (PHG_REPL_OWN)
+#if PHG_REPL_OWN
+        uint32_t cb0 = 0, cb1 = 0, cb2 = 0, cb3 = 0;  // candidate shift register
+#endif
 #if PHG_VSYM
         // same-column pairs for the first rows: up[d-1] = (ylo-d, ylo);
         // pend[d-2][q] = (ylo+1+q-d, ylo+1+q) for rows ylo+1+q, q < d-1
