@@ -339,10 +339,10 @@ __global__ void __launch_bounds__(kH2Threads, 2)
             fl_n = rp_n = 0;
         };
         int pending = 0;  // warp-uniform: items waiting at ring[0, pending)
-        // process ring[h, h+n), n <= 64: two independent candidates per lane
+        // process ring[h, h+n), n <= kH2Round: three independent candidates per
+        // lane, all loads issued before any store.  Items are the byte offsets
+        // of the candidates in the interleaved tile.
         auto drain = [&](int h, int n) {
-            // item = quad << 10 | lane << 5 | bit (quad = first row / 4)
-            // items are byte offsets of candidates in the interleaved tile
             const int o0 = static_cast<int>(lds16(ring + 2 * (h + (lane < n ? lane : 0))));
             const int o1 = static_cast<int>(lds16(ring + 2 * (h + (lane + 32 < n ? lane + 32 : 0))));
             const int o2 = static_cast<int>(lds16(ring + 2 * (h + (lane + 64 < n ? lane + 64 : 0))));
