@@ -9,9 +9,13 @@ launching stream after warm-up; one JSON line per op.
                 algorithmic bytes 1 B in per pixel
   sse           phg_dev_sse (exact uint64 numerator of mse)
                 algorithmic bytes 2 B in per pixel
+  removal       phg_dev_removal (denoise_pass with a caller-supplied int32
+                map, denoise.hpp:243-283): 1 B image + 4 B map in, 1 B out
 
 Workloads: the c4 batch (4096 x 481x321 = 632 Mpx) and one 16384^2 image
-(268 Mpx), both larger than L2.  Synthetic inputs (uniform random bytes).
+(268 Mpx), both larger than L2.  Synthetic inputs (uniform random bytes):
+for `removal` that is the worst case, ~2/3 of the pixels flagged by the map
+(a denoise-stream map flags 10-30%).
 
     python bench_ops.py [--reps 20]
 """
@@ -33,7 +37,7 @@ def main():
     a = ap.parse_args()
     import torch
 
-    from paper_1306_5390_b200._lib import PhgDevImage, check, lib
+    from paper_1306_5390_b200._lib import PhgDevImage, PhgParams, check, lib
 
     L = lib()
     dev = torch.device("cuda:0")
@@ -73,6 +77,9 @@ def main():
         cpitch = (w + 3) // 4 * 4
         card = torch.empty((n, h, cpitch), dtype=torch.int32, device=dev)
         cnt = torch.zeros(n, dtype=torch.int64, device=dev)
+        ctr = torch.zeros((n, 1, 2), dtype=torch.int64, device=dev)
+        iz = dev_image(y, w, h, n)
+        params = PhgParams(20, 1, 1, 3, 0)
         px = n * w * h
         ops = {
             "cardinality": (5.0, lambda: check(L.phg_dev_cardinality(C.byref(ix), 20, 1, C.c_void_p(card.data_ptr()),
@@ -80,6 +87,9 @@ def main():
             "residual": (1.0, lambda: check(L.phg_dev_residual_count(C.byref(ix), 20, 1, 3,
                                                                      C.c_void_p(cnt.data_ptr()), sh))),
             "sse": (2.0, lambda: check(L.phg_dev_sse(C.byref(ix), C.byref(iy), C.c_void_p(cnt.data_ptr()), sh))),
+            "removal": (6.0, lambda: check(L.phg_dev_removal(C.byref(ix), C.c_void_p(card.data_ptr()), cpitch,
+                                                             C.byref(params), C.byref(iz),
+                                                             C.c_void_p(ctr.data_ptr()), sh))),
         }
         for name, (bpp, fn) in ops.items():
             ms = timed(fn)

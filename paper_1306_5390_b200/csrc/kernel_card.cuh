@@ -272,4 +272,132 @@ __global__ void __launch_bounds__(256) count_lt_kernel(const int32_t* card, int6
     if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&counts[img], (unsigned long long)cnt);
 }
 
+// ---------------------------------------------------------------------------
+// denoise_pass with a caller-supplied cardinality map, beta = 1
+// (removal_rows, denoise.hpp:171-223): flagged <=> map < thr (the map is
+// honoured as given, never recomputed); a flagged pixel's 3x3 window gives
+// the dissimilar count and sum of squares; replace if flag > pix_count - 3
+// and flag > 0.  One thread per 4-pixel word of one row; the block stages
+// its 256 x 16 tile plus a 1-row / 16-px apron in shared memory (zeros
+// outside the image, corrected by the in-bounds count as in the fused
+// kernel), reads the map as int4 and writes 4-byte words.  Per pixel: 1 B in,
+// 4 B map in, 1 B out.
+struct RemovalArgs {
+    const uint8_t* src;
+    uint8_t* dst;
+    const int32_t* card;
+    int64_t card_pitch;    // elements
+    int64_t card_stride;   // elements per image
+    int64_t pitch;         // image bytes per row (src and dst)
+    int64_t image_stride;
+    int width, height;
+    int alpha, thr, faithful;
+    uint32_t k7;           // ((256-alpha) & 0x7f) in every byte
+    unsigned long long* counters;  // [n][1][2]
+};
+
+constexpr int kRmTW = 256;          // tile width (px)
+constexpr int kRmTH = 16;           // tile height (rows)
+constexpr int kRmSP = kRmTW + 32;   // staged row pitch: 16-px aprons
+
+template <bool ALE, bool VEC>
+__global__ void __launch_bounds__(256) removal_b1_kernel(const RemovalArgs a) {
+    __shared__ __align__(16) uint8_t tile[(kRmTH + 2) * kRmSP];
+    const int img = blockIdx.z;
+    const int x0 = blockIdx.x * kRmTW, y0 = blockIdx.y * kRmTH;
+    const uint8_t* src = a.src + img * a.image_stride;
+    // stage rows y0-1 .. y0+kRmTH, columns x0-16 .. x0+kRmTW+16 (zeros outside)
+    for (int i = threadIdx.x; i < (kRmTH + 2) * (kRmSP / 16); i += 256) {
+        const int r = i / (kRmSP / 16), ch = i - r * (kRmSP / 16);
+        const int gy = y0 - 1 + r, gx = x0 - 16 + 16 * ch;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (gy >= 0 && gy < a.height && gx >= 0 && gx < a.width) {
+            v = *reinterpret_cast<const uint4*>(src + gy * a.pitch + gx);
+            const int valid = a.width - gx;  // bytes past the width are pitch padding
+            if (valid < 16) {
+                uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int nb = min(max(valid - 4 * k, 0), 4);
+                    w[k] &= nb == 4 ? 0xffffffffu : ((1u << (8 * nb)) - 1u);
+                }
+                v = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+        }
+        *reinterpret_cast<uint4*>(tile + r * kRmSP + 16 * ch) = v;
+    }
+    __syncthreads();
+    const int wcol = threadIdx.x & 63;   // word column
+    const int rg = threadIdx.x >> 6;     // 4 row groups of 4 rows
+    const int gx = x0 + 4 * wcol;
+    unsigned fl = 0, rp = 0;
+    if (gx < a.width) {
+        const int nvalid = min(4, a.width - gx);
+        for (int rr = 0; rr < kRmTH / 4; ++rr) {
+            const int ly = rg * (kRmTH / 4) + rr;  // tile row
+            const int gy = y0 + ly;
+            if (gy >= a.height) break;
+            const int32_t* cp = a.card + img * a.card_stride + gy * a.card_pitch + gx;
+            int cv[4];
+            if (VEC && nvalid == 4) {
+                const int4 c4 = *reinterpret_cast<const int4*>(cp);
+                cv[0] = c4.x; cv[1] = c4.y; cv[2] = c4.z; cv[3] = c4.w;
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) cv[j] = j < nvalid ? cp[j] : 0x7fffffff;
+            }
+            const uint8_t* c0 = tile + (ly + 1) * kRmSP + 16 + 4 * wcol;  // this word, staged
+            uint32_t out = *reinterpret_cast<const uint32_t*>(c0);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (cv[j] >= a.thr) continue;
+                ++fl;
+                // 3x3 window of lane j: three funnel-shifted row words
+                uint32_t R[3];
+#pragma unroll
+                for (int r = 0; r < 3; ++r) {
+                    const uint8_t* rp0 = c0 + (r - 1) * kRmSP;
+                    const uint32_t lo = *reinterpret_cast<const uint32_t*>(rp0 - 4);
+                    const uint32_t mid = *reinterpret_cast<const uint32_t*>(rp0);
+                    const uint32_t hi = *reinterpret_cast<const uint32_t*>(rp0 + 4);
+                    // bytes j-1, j, j+1 of the word at lane 0
+                    R[r] = j == 0 ? __funnelshift_l(lo, mid, 8) : __funnelshift_r(mid, hi, 8 * (j - 1));
+                }
+                const uint32_t n1 = prmt(R[0], R[1], 0x4210);  // t0 t1 t2 m0
+                const uint32_t n2 = prmt(R[1], R[2], 0x6542);  // m2 b0 b1 b2
+                const uint32_t p4 = prmt(R[1], 0, 0x1111);
+                const uint32_t d1 = __vabsdiffu4(n1, p4), d2 = __vabsdiffu4(n2, p4);
+                const uint32_t t1 = (d1 & kLo7) + a.k7, t2 = (d2 & kLo7) + a.k7;
+                const uint32_t dis1 = (ALE ? (d1 | t1) : (d1 & t1)) & kHi;
+                const uint32_t dis2 = (ALE ? (d2 | t2) : (d2 & t2)) & kHi;
+                const int fc = __popc(dis1 | (dis2 >> 1));
+                const uint32_t S = __dp4a(n2 & msb_to_bytes(dis2), n2, __dp4a(n1 & msb_to_bytes(dis1), n1, 0u));
+                const int p = (R[1] >> 8) & 0xff;
+                const int gxj = gx + j;
+                const int inb = (3 - (gy == 0) - (gy == a.height - 1)) * (3 - (gxj == 0) - (gxj == a.width - 1));
+                // cells outside the image are 0 in the tile: dissimilar exactly when p >= alpha
+                const int f = fc - (p >= a.alpha ? 9 - inb : 0);
+                const int pix_count = a.faithful ? 9 : inb;
+                if (f > pix_count - 3 && f > 0) {
+                    const uint32_t v = rms_round32(S, static_cast<uint32_t>(f));
+                    out = (out & ~(0xffu << (8 * j))) | (v << (8 * j));
+                    ++rp;
+                }
+            }
+            uint8_t* dp = a.dst + img * a.image_stride + gy * a.pitch + gx;
+            if (nvalid == 4) {
+                *reinterpret_cast<uint32_t*>(dp) = out;
+            } else {
+                for (int j = 0; j < nvalid; ++j) dp[j] = static_cast<uint8_t>(out >> (8 * j));
+            }
+        }
+    }
+    fl = __reduce_add_sync(0xffffffffu, fl);
+    rp = __reduce_add_sync(0xffffffffu, rp);
+    if ((threadIdx.x & 31) == 0 && a.counters) {
+        if (fl) atomicAdd(&a.counters[img * 2], (unsigned long long)fl);
+        if (rp) atomicAdd(&a.counters[img * 2 + 1], (unsigned long long)rp);
+    }
+}
+
 }  // namespace phg

@@ -847,6 +847,46 @@ int phg_dev_sse(const phg_dev_image* a, const phg_dev_image* b, uint64_t* sse, v
 int phg_dev_removal(const phg_dev_image* src, const int32_t* card, int64_t card_pitch, const phg_params* p,
                     const phg_dev_image* dst, uint64_t* counters, void* stream) {
     PHG_TRY(validate(p));
+    if (p->beta == 1 && !getenv("PHG_NO_H2")) {
+        // tiled byte-SIMD pass (kernel_card.cuh removal_b1_kernel)
+        if ((reinterpret_cast<uintptr_t>(src->data) | reinterpret_cast<uintptr_t>(dst->data) | src->pitch |
+             src->image_stride) & 15 || src->pitch != dst->pitch || src->image_stride != dst->image_stride)
+            return fail(PHG_EINVAL, "device images must be 16-byte aligned with 16-byte pitches");
+        phg::RemovalArgs a;
+        a.src = src->data;
+        a.dst = dst->data;
+        a.card = card;
+        a.card_pitch = card_pitch;
+        a.card_stride = card_pitch * src->rows;
+        a.pitch = src->pitch;
+        a.image_stride = src->image_stride;
+        a.width = src->width;
+        a.height = src->rows;
+        a.alpha = p->alpha;
+        a.thr = p->card_threshold;
+        a.faithful = p->border == PHG_BORDER_FAITHFUL;
+        a.k7 = ((256u - static_cast<uint32_t>(p->alpha)) & 0x7fu) * 0x01010101u;
+        a.counters = reinterpret_cast<unsigned long long*>(counters);
+        const bool vec = (card_pitch & 3) == 0 && (reinterpret_cast<uintptr_t>(card) & 15) == 0;
+        const bool ale = p->alpha <= 128;
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        for (int z0 = 0; z0 < src->n_images; z0 += 65535) {
+            phg::RemovalArgs a2 = a;
+            a2.src += z0 * src->image_stride;
+            a2.dst += z0 * src->image_stride;
+            a2.card += z0 * a.card_stride;
+            if (a2.counters) a2.counters += static_cast<int64_t>(z0) * 2;
+            dim3 grid((src->width + phg::kRmTW - 1) / phg::kRmTW, (src->rows + phg::kRmTH - 1) / phg::kRmTH,
+                      std::min(65535, src->n_images - z0));
+            if (ale && vec) phg::removal_b1_kernel<true, true><<<grid, 256, 0, st>>>(a2);
+            else if (ale) phg::removal_b1_kernel<true, false><<<grid, 256, 0, st>>>(a2);
+            else if (vec) phg::removal_b1_kernel<false, true><<<grid, 256, 0, st>>>(a2);
+            else phg::removal_b1_kernel<false, false><<<grid, 256, 0, st>>>(a2);
+            ++g_launches;
+            PHG_CUDA(cudaGetLastError());
+        }
+        return PHG_OK;
+    }
     return launch_scalar(phg::kModeRemoval, *src, dst, card, nullptr, card_pitch, 0, src->rows, 0,
                          src->rows, *p, 0, counters, 1, static_cast<cudaStream_t>(stream));
 }

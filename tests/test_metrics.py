@@ -96,3 +96,22 @@ def test_cardmap_p2_on_gpu():
     imp.set(1, 1, 255)
     assert P.cardmap(imp) == "P2\n3 3\n9\n3 5 3\n5 1 5\n3 5 3\n"
     assert P.cardmap(G(3, 3, 100), beta=2)[:9] == "P2\n3 3\n25"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("alpha", [1, 20, 200])
+@pytest.mark.parametrize("border", [0, 1])
+def test_denoise_pass_tiled_beta1_vs_oracle(alpha, border):
+    # denoise_pass with a caller-supplied map (denoise.hpp:243-283) on the
+    # tiled beta=1 kernel: multi-tile shapes, the true map and arbitrary maps
+    rng = np.random.default_rng(alpha * 7 + border)
+    for w, h in ((700, 301), (257, 17), (1023, 64)):
+        img = O.inject_sp_noise(O.synth_image(w, h, w + h), 0.3, 0.5, alpha)
+        for kind in ("true", "random"):
+            card = O.cardinality(img, alpha, 1) if kind == "true" else rng.integers(0, 10, (h, w)).astype(np.int32)
+            for thr in (1, 3, 7):
+                p = P.DenoiseParams(alpha, 1, 1, thr, P.BorderMode(border))
+                out, st = P.denoise_pass(G.from_array(img), P.CardinalityMap(w, h, card.reshape(-1)), p)
+                ref, f, r = O.removal_pass(img, card, alpha, 1, thr, border)
+                assert np.array_equal(out.pixels, ref), (w, h, kind, thr)
+                assert (st.flagged, st.replaced) == (f, r)
