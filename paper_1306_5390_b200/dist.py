@@ -113,9 +113,11 @@ def denoise_band(src: torch.Tensor, tmp_a: torch.Tensor, tmp_b: torch.Tensor, pl
     tmp_a/tmp_b (whose halo rows are refreshed after every launch)."""
     cur, nxt = src, tmp_a
     it0 = 0
-    for i, iters in enumerate(chunk_plan(k, tmax)):
+    launches = chunk_plan(k, tmax)
+    for i, iters in enumerate(launches):
         stepper(cur, nxt, plan, it0, iters)
-        exchange_halos(nxt, plan, group)
+        if i + 1 < len(launches):  # the last launch's halos are never read
+            exchange_halos(nxt, plan, group)
         cur = nxt
         nxt = tmp_b if nxt is tmp_a else tmp_a
         it0 += iters
