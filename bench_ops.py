@@ -87,6 +87,8 @@ def main():
             "residual": (1.0, lambda: check(L.phg_dev_residual_count(C.byref(ix), 20, 1, 3,
                                                                      C.c_void_p(cnt.data_ptr()), sh))),
             "sse": (2.0, lambda: check(L.phg_dev_sse(C.byref(ix), C.byref(iy), C.c_void_p(cnt.data_ptr()), sh))),
+            "cardinality_beta2": (5.0, lambda: check(L.phg_dev_cardinality(C.byref(ix), 20, 2,
+                                                                           C.c_void_p(card.data_ptr()), cpitch, sh))),
             "removal": (6.0, lambda: check(L.phg_dev_removal(C.byref(ix), C.c_void_p(card.data_ptr()), cpitch,
                                                              C.byref(params), C.byref(iz),
                                                              C.c_void_p(ctr.data_ptr()), sh))),

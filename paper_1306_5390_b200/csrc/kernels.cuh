@@ -103,6 +103,9 @@ struct TileArgs {
     int kcap;
     unsigned long long* counters;  // [n_images][kcap][2]
     uint32_t one;                  // runtime 1 (keeps IMAD adds on the FMA pipe)
+    int32_t* card_out;             // CARD mode: [n][rows][card_pitch] (rows from row_base)
+    int64_t card_pitch;            // elements
+    int64_t card_stride;           // elements per image
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -365,7 +368,10 @@ __device__ __forceinline__ uint32_t count_similar_vs(const uint32_t (&win)[2 * B
     return cnt;
 }
 
-template <int BETA, int T, bool ALE>
+// CARD = true: one cardinality pass (compute_cardinality, denoise.hpp:
+// 227-241) -- the same staged sweep, the per-lane counts C written as int32
+// for the owned in-image pixels, no removal.
+template <int BETA, int T, bool ALE, bool CARD = false>
 __global__ void __launch_bounds__(kThreads)
     fused_tb_kernel(const __grid_constant__ CUtensorMap src_map, const TileArgs a) {
     static_assert(BETA * T <= kMaxHaloPx, "halo exceeds the staged columns");
@@ -514,36 +520,50 @@ __global__ void __launch_bounds__(kThreads)
             const uint32_t cnt = count_similar<BETA, ALE, ROWS_OK>(win, colm, rowm, a.k7, a.one);
 #endif
             const uint32_t card = cnt + 0x01010101u;
-            const uint32_t inimg = row_in ? inimg_col : 0u;
-            const uint32_t flagged = lt_bits(card, a.k_thr) & inimg;
-            // interior: in_bounds = pix_count = (2B+1)^2, so
-            // flag > pix_count-3 <=> card < 3 (and flag > 0 holds); border
-            // words defer the whole decision to the replacement pass.
-            const bool interior = ROWS_OK && !col_border;
-            const uint32_t cand = interior ? (flagged & lt_bits(card, rep4(125u))) : flagged;
-            constexpr bool kTag = PHG_INTERIOR_TAG;
-            // pixels outside the image are kept at 0 (see process_pixel)
-            *reinterpret_cast<uint32_t*>(dstb + y * kRP + 4 * w) =
-                win[BETA][BETA] & (row_in ? inimg_bytes : 0u);
-            // bits 7,15,23,31 -> nibble (no carries: the shifted copies never overlap)
+            if constexpr (CARD) {
+                if (y >= HALO && y < HALO + out_rows && own_word && row_in) {
+                    int32_t* o = a.card_out + img * a.card_stride +
+                                 static_cast<int64_t>(gy0 + y - a.row_base) * a.card_pitch + gcol;
+                    const int nv = min(4, a.width - gcol);
+                    if (nv == 4 && (a.card_pitch & 3) == 0) {
+                        *reinterpret_cast<int4*>(o) = make_int4(card & 0xff, (card >> 8) & 0xff, (card >> 16) & 0xff,
+                                                               card >> 24);
+                    } else {
+                        for (int l = 0; l < nv; ++l) o[l] = (card >> (8 * l)) & 0xff;
+                    }
+                }
+            } else {
+                const uint32_t inimg = row_in ? inimg_col : 0u;
+                const uint32_t flagged = lt_bits(card, a.k_thr) & inimg;
+                // interior: in_bounds = pix_count = (2B+1)^2, so
+                // flag > pix_count-3 <=> card < 3 (and flag > 0 holds); border
+                // words defer the whole decision to the replacement pass.
+                const bool interior = ROWS_OK && !col_border;
+                const uint32_t cand = interior ? (flagged & lt_bits(card, rep4(125u))) : flagged;
+                constexpr bool kTag = PHG_INTERIOR_TAG;
+                // pixels outside the image are kept at 0 (see process_pixel)
+                *reinterpret_cast<uint32_t*>(dstb + y * kRP + 4 * w) =
+                    win[BETA][BETA] & (row_in ? inimg_bytes : 0u);
+                // bits 7,15,23,31 -> nibble (no carries: the shifted copies never overlap)
 #if PHG_REPL_OWN
-            // this thread's own candidates: 4 bits per row pushed into a
-            // 128-bit shift register (rows per group <= 32)
-            {
-                const uint32_t nib = (cand * 0x00204081u) >> 28;
-                cb3 = __funnelshift_l(cb2, cb3, 4);
-                cb2 = __funnelshift_l(cb1, cb2, 4);
-                cb1 = __funnelshift_l(cb0, cb1, 4);
-                cb0 = (cb0 << 4) | nib;
-            }
+                // this thread's own candidates: 4 bits per row pushed into a
+                // 128-bit shift register (rows per group <= 32)
+                {
+                    const uint32_t nib = (cand * 0x00204081u) >> 28;
+                    cb3 = __funnelshift_l(cb2, cb3, 4);
+                    cb2 = __funnelshift_l(cb1, cb2, 4);
+                    cb1 = __funnelshift_l(cb0, cb1, 4);
+                    cb0 = (cb0 << 4) | nib;
+                }
 #else
-            // + bit 4: the word's candidates are decided interior replacements
-            cmap[y * kCompWords + (w - kFirstWord)] =
-                static_cast<uint8_t>(((cand * 0x00204081u) >> 28) | (kTag && interior ? 0x10u : 0u));
+                // + bit 4: the word's candidates are decided interior replacements
+                cmap[y * kCompWords + (w - kFirstWord)] =
+                    static_cast<uint8_t>(((cand * 0x00204081u) >> 28) | (kTag && interior ? 0x10u : 0u));
 #endif
-            if (y >= HALO && y < HALO + out_rows) {
-                fl_acc += (flagged & own_col) >> 7;
-                if (kTag && interior) rp_acc += (cand & own_col) >> 7;
+                if (y >= HALO && y < HALO + out_rows) {
+                    fl_acc += (flagged & own_col) >> 7;
+                    if (kTag && interior) rp_acc += (cand & own_col) >> 7;
+                }
             }
 #pragma unroll
             for (int i = 0; i < NB - 1; ++i)
@@ -554,6 +574,7 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll 3
         for (int y = yint_lo; y < yint_hi; ++y) row(y, std::true_type{});
         for (int y = yint_hi; y < yhi; ++y) row(y, std::false_type{});
+        if constexpr (CARD) continue;  // T == 1: the map is written, nothing else
         nfl[t] += __dp4a(fl_acc, 0x01010101u, 0u);
         nrp[t] += __dp4a(rp_acc, 0x01010101u, 0u);
 #if PHG_REPL_OWN
@@ -666,6 +687,7 @@ __global__ void __launch_bounds__(kThreads)
         __syncthreads();
     }
 
+    if constexpr (CARD) return;
     // owned output rows: shared -> global, 16-byte coalesced stores
     {
         const uint8_t* fin = buf[T & 1];

@@ -334,6 +334,65 @@ int launch_card_h2(const phg_dev_image& src, int alpha, int mode, int thr, int32
     return PHG_OK;
 }
 
+// compute_cardinality for beta >= 2 (and beta = 1 under PHG_NO_H2) on the
+// byte-SIMD kernel in CARD mode: one staged sweep, int32 C per pixel.
+int launch_card_tb(const phg_dev_image& src, int alpha, int beta, int32_t* card, int64_t card_pitch,
+                   cudaStream_t stream) {
+    const bool ale = alpha <= 128;
+    FusedFn fn = nullptr;
+    if (beta == 1) fn = ale ? phg::fused_tb_kernel<1, 1, true, true> : phg::fused_tb_kernel<1, 1, false, true>;
+    if (beta == 2) fn = ale ? phg::fused_tb_kernel<2, 1, true, true> : phg::fused_tb_kernel<2, 1, false, true>;
+    if (!fn) return fail(PHG_EINVAL, "no staged cardinality kernel for this beta");
+    const Launch L = plan_rows(src.rows, beta, generic_rows_target());
+    const int sh = L.th + 2 * beta;
+    if (sh > 64) return fail(PHG_EINVAL, "tile too tall");
+    const size_t smem = phg::smem_bytes(sh);
+    CUtensorMap map;
+    PHG_TRY(encode_map(&map, src, sh));
+    PHG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    phg::TileArgs a{};
+    a.dst = nullptr;
+    a.pitch = src.pitch;
+    a.image_stride = src.image_stride;
+    a.width = src.width;
+    a.height = src.rows;
+    a.row_base = 0;
+    a.own_lo = 0;
+    a.own_hi = src.rows;
+    a.th = L.th;
+    a.k7 = ((256u - static_cast<uint32_t>(alpha)) & 0x7fu) * 0x01010101u;
+    a.k_thr = (128u - 3u) * 0x01010101u;
+    a.alpha = alpha;
+    a.thr = 3;
+    a.faithful = 1;
+    a.it0 = 0;
+    a.kcap = 1;
+    a.counters = nullptr;
+    a.one = 1u;
+    a.card_out = card;
+    a.card_pitch = card_pitch;
+    a.card_stride = card_pitch * src.rows;
+    const int tiles_x = (src.width + phg::kOutPx - 1) / phg::kOutPx;
+    for (int z0 = 0; z0 < src.n_images; z0 += 65535) {
+        const int nz = std::min(65535, src.n_images - z0);
+        CUtensorMap m2 = map;
+        phg::TileArgs a2 = a;
+        if (z0) {
+            phg_dev_image s2 = src;
+            s2.data += z0 * src.image_stride;
+            s2.n_images = nz;
+            PHG_TRY(encode_map(&m2, s2, sh));
+            a2.card_out += static_cast<int64_t>(z0) * a.card_stride;
+        }
+        dim3 grid(tiles_x, L.tiles_y, nz);
+        fn<<<grid, phg::kThreads, smem, stream>>>(m2, a2);
+        ++g_launches;
+        PHG_CUDA(cudaGetLastError());
+    }
+    return PHG_OK;
+}
+
 int launch_fused(const phg_dev_image& src, const phg_dev_image& dst, int row_base, int height,
                  int own_lo, int own_hi, const phg_params& p, int it0, int iters,
                  uint64_t* counters, int kcap, cudaStream_t stream) {
@@ -797,6 +856,7 @@ int phg_dev_cardinality(const phg_dev_image* src, int alpha, int beta, int32_t* 
     if (beta == 1 && !getenv("PHG_NO_H2"))
         return launch_card_h2(*src, alpha, phg::kCardMap, 1, card, card_pitch, nullptr,
                               static_cast<cudaStream_t>(stream));
+    if (beta <= 2) return launch_card_tb(*src, alpha, beta, card, card_pitch, static_cast<cudaStream_t>(stream));
     return launch_scalar(phg::kModeCard, *src, nullptr, nullptr, card, card_pitch, 0, src->rows, 0,
                          src->rows, p, 0, nullptr, 1, static_cast<cudaStream_t>(stream));
 }
