@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c4", choices=["c4", "c2", "c1", "c3", "c5"])
     ap.add_argument("--c5-size", type=int, default=65536, help="c5 image side (parity runs use less)")
+    ap.add_argument("--gen", default="reference", choices=["reference", "device"],
+                    help="c5 input: the reference generators per 4096^2 tile on the host, or the on-device "
+                         "counter-based generators (phg_dev_synth_smooth + phg_dev_inject_noise)")
     ap.add_argument("--images", type=int, default=4096, help="images per rank (c4)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="images in the CPU sample (0=auto)")
@@ -382,9 +385,16 @@ def run_bands(R, a):
     pitch = (S + 15) // 16 * 16
     params = PhgParams(ALPHA, beta, K, 3, 0)
     host = torch.empty((plan.rows, S), dtype=torch.uint8, pin_memory=True)
-    WL.c5_rows(plan.blo, plan.bhi, S, min(WL.C5_TILE, S), out=host.numpy())
     bufs = [torch.zeros((plan.rows, pitch), dtype=torch.uint8, device=R.dev) for _ in range(3)]
-    bufs[0][:, :S].copy_(host.to(R.dev))
+    if a.gen == "device":
+        gim = dev_image(bufs[0], S, plan.rows, 1)
+        R.check(L.phg_dev_synth_smooth(C.byref(gim), plan.blo, S, 1, C.c_void_p(R.sh)))
+        R.check(L.phg_dev_inject_noise(C.byref(gim), plan.blo, S, 0.30, 0.5, 12345, None, C.c_void_p(R.sh)))
+        torch.cuda.synchronize()
+        host.copy_(bufs[0][:, :S])
+    else:
+        WL.c5_rows(plan.blo, plan.bhi, S, min(WL.C5_TILE, S), out=host.numpy())
+        bufs[0][:, :S].copy_(host.to(R.dev))
     counters = torch.zeros((K, 2), dtype=torch.int64, device=R.dev)
     stepper = D.cuda_band_stepper(params, counters, S, S, R.sh)
     group = None
@@ -434,7 +444,9 @@ def run_bands(R, a):
     cfg = {"workload": "c5: " + c5_desc(a), "width": S, "height": S, "alpha": ALPHA, "beta": beta, "k": K,
            "card_threshold": 3, "border": "Faithful", "band_rows_per_rank": plan.hi - plan.lo,
            "halo_rows": beta * tmax, "parallelism": f"row bands x{R.world}, NCCL halo send/recv per launch",
-           "l2": "inputs larger than L2", "generator": "per-4096^2-tile reference generators (DESIGN.md)"}
+           "l2": "inputs larger than L2",
+           "generator": ("on-device counter-based generators (kernel_gen.cuh, DESIGN.md)" if a.gen == "device"
+                         else "per-4096^2-tile reference generators (DESIGN.md)")}
     e2e = {"value": round(pix_it * R.world * e2e_steps / e2e_s / 1e6, 3), "unit": UNIT,
            "h2d_bytes_per_step": plan.rows * S, "d2h_bytes_per_step": (plan.hi - plan.lo) * S + K * 2 * 8,
            "path": e2e_path}

@@ -178,6 +178,19 @@ int phg_dev_residual_count(const phg_dev_image* img, int alpha, int beta, int ca
                            uint64_t* counts, void* stream);
 int phg_dev_sse(const phg_dev_image* a, const phg_dev_image* b, uint64_t* sse, void* stream);
 
+/* On-device, counter-based input generators for giga-pixel workloads
+ * (kernel_gen.cuh).  The same structure as the
+ * reference's SmoothRandom synth_image (white noise + clamped 3x3 mean) and
+ * salt-and-pepper injection, but every pixel is a pure function of (seed,
+ * image, row, column): NOT bit-equal to the mt19937 generators, and the noise
+ * is Bernoulli(density) per pixel (expected, not exact, count).  The
+ * buffer holds global rows [row_base, row_base + rows) of images `height`
+ * rows tall (a row band; 0 and rows for whole images).  count (device
+ * uint64, may be null) accumulates the corrupted pixels. */
+int phg_dev_synth_smooth(const phg_dev_image* out, int row_base, int height, uint64_t seed, void* stream);
+int phg_dev_inject_noise(const phg_dev_image* img, int row_base, int height, double density,
+                         double salt_ratio, uint64_t seed, uint64_t* count, void* stream);
+
 /* Turn device counters into reference PassStats: per image, truncate after
  * the first iteration with replaced == 0 (denoise.hpp:308). */
 int phg_finalize_stats(const uint64_t* host_counters, int n_images, int kcap,

@@ -13,6 +13,7 @@ Two libraries:
 from __future__ import annotations
 
 import ctypes as C
+import math
 import os
 import subprocess
 
@@ -227,3 +228,61 @@ def ref_denoise_batch(imgs, alpha=20, beta=1, k=5, thr=3, border=0, threads=1):
     its = np.zeros(n, np.int32)
     ref().ref_denoise_batch(imgs, n, w, h, alpha, beta, k, thr, border, threads, out, its)
     return out, its
+
+
+# ---------------------------------------------------------------------------
+# The on-device counter-based generators (kernel_gen.cuh)
+# restated in numpy.  These are NEW generators (not the reference's mt19937
+# streams); this restatement is their parity checker.
+_M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+def _mix64(z):
+    z = np.asarray(z, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = z + np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
+
+
+def _gen_index(n, h, w):
+    img = np.arange(n, dtype=np.uint64)[:, None, None]
+    r = np.arange(h, dtype=np.uint64)[None, :, None]
+    c = np.arange(w, dtype=np.uint64)[None, None, :]
+    with np.errstate(over="ignore"):
+        return (img * np.uint64(h) + r) * np.uint64(w) + c
+
+
+def dev_smooth(w, h, seed, n=1):
+    """phg_dev_synth_smooth: field = mix64(seed*K + index) & 0xff, then the
+    clamped 3x3 mean with round-half-up (image.hpp:87-101 smoothing)."""
+    with np.errstate(over="ignore"):
+        base = np.uint64(seed) * np.uint64(0xD1342543DE82EF95)
+        field = (_mix64(base + _gen_index(n, h, w)) & np.uint64(0xFF)).astype(np.int64)
+    pad = np.pad(field, ((0, 0), (1, 1), (1, 1)))
+    ones = np.pad(np.ones((n, h, w), np.int64), ((0, 0), (1, 1), (1, 1)))
+    s = sum(pad[:, 1 + dy:1 + dy + h, 1 + dx:1 + dx + w] for dy in (-1, 0, 1) for dx in (-1, 0, 1))
+    cnt = sum(ones[:, 1 + dy:1 + dy + h, 1 + dx:1 + dx + w] for dy in (-1, 0, 1) for dx in (-1, 0, 1))
+    return ((s + cnt // 2) // cnt).astype(np.uint8)
+
+
+def dev_noise(imgs, density, salt_ratio, seed):
+    """phg_dev_inject_noise: Bernoulli(density) per pixel from
+    mix64(seed*K + index), salt iff mix64(draw) < salt_ratio * 2^64."""
+    imgs = np.array(imgs, dtype=np.uint8, copy=True)
+    if imgs.ndim == 2:
+        imgs = imgs[None]
+    n, h, w = imgs.shape
+    if density == 0.0:
+        return imgs, 0
+    with np.errstate(over="ignore"):
+        base = np.uint64(seed) * np.uint64(0xD1342543DE82EF95)
+        u = _mix64(base + _gen_index(n, h, w))
+    hit = np.ones_like(u, dtype=bool) if density >= 1.0 else u < np.uint64(int(math.ldexp(density, 64)))
+    if salt_ratio >= 1.0:
+        salt = np.ones_like(hit)
+    else:
+        salt = _mix64(u) < np.uint64(int(math.ldexp(salt_ratio, 64)))
+    imgs[hit] = np.where(salt[hit], 255, 0).astype(np.uint8)
+    return imgs, int(hit.sum())

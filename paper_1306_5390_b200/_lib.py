@@ -24,6 +24,7 @@ EXPORTS = (
     "phg_inject_sp_noise", "phg_max_fused_iterations", "phg_dev_fused_step",
     "phg_dev_denoise", "phg_dev_cardinality", "phg_dev_removal", "phg_finalize_stats",
     "phg_fused_kernel_name", "phg_residual_noise_count", "phg_sse", "phg_dev_residual_count", "phg_dev_sse",
+    "phg_dev_synth_smooth", "phg_dev_inject_noise",
 )
 
 
@@ -103,6 +104,9 @@ def lib():
         L.phg_dev_residual_count.argtypes = [C.POINTER(PhgDevImage), C.c_int, C.c_int, C.c_int, C.c_void_p,
                                              C.c_void_p]
         L.phg_dev_sse.argtypes = [C.POINTER(PhgDevImage), C.POINTER(PhgDevImage), C.c_void_p, C.c_void_p]
+        L.phg_dev_synth_smooth.argtypes = [C.POINTER(PhgDevImage), C.c_int, C.c_int, C.c_uint64, C.c_void_p]
+        L.phg_dev_inject_noise.argtypes = [C.POINTER(PhgDevImage), C.c_int, C.c_int, C.c_double, C.c_double,
+                                           C.c_uint64, C.c_void_p, C.c_void_p]
         _LIB = L
     return _LIB
 

@@ -24,6 +24,7 @@
 #include "../../include/phgrms_b200.h"
 #include "kernel_b1.cuh"
 #include "kernel_card.cuh"
+#include "kernel_gen.cuh"
 #include "kernel_h2.cuh"
 #include "kernels.cuh"
 
@@ -968,6 +969,59 @@ int phg_cardinality(const uint8_t* img, int w, int h, int alpha, int beta, int32
     PHG_CUDA(cudaMemcpy2DAsync(counts, sizeof(int32_t) * w, pc, sizeof(int32_t) * cpitch,
                                sizeof(int32_t) * w, h, cudaMemcpyDeviceToHost, s->stream));
     PHG_CUDA(cudaStreamSynchronize(s->stream));
+    return PHG_OK;
+}
+
+int phg_dev_synth_smooth(const phg_dev_image* out, int row_base, int height, uint64_t seed, void* stream) {
+    if (!out || !out->data) return fail(PHG_EINVAL, "null argument");
+    PHG_TRY(check_dims(out->width, out->rows));
+    if (row_base < 0 || row_base + out->rows > height) return fail(PHG_EINVAL, "rows outside the image");
+    if (out->n_images < 1 || out->n_images > 65535) return fail(PHG_EINVAL, "1..65535 images per call");
+    phg::GenArgs a{};
+    a.img = out->data;
+    a.pitch = out->pitch;
+    a.image_stride = out->image_stride;
+    a.width = out->width;
+    a.rows = out->rows;
+    a.n = out->n_images;
+    a.row_base = row_base;
+    a.height = height;
+    a.seed = seed;
+    dim3 grid((out->width + 255) / 256, std::min(out->rows, 65535), out->n_images);
+    phg::gen_smooth_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
+    ++g_launches;
+    PHG_CUDA(cudaGetLastError());
+    return PHG_OK;
+}
+
+int phg_dev_inject_noise(const phg_dev_image* img, int row_base, int height, double density, double salt_ratio,
+                         uint64_t seed, uint64_t* count, void* stream) {
+    if (!img || !img->data) return fail(PHG_EINVAL, "null argument");
+    if (row_base < 0 || row_base + img->rows > height) return fail(PHG_EINVAL, "rows outside the image");
+    if (!(density >= 0.0 && density <= 1.0)) return fail(PHG_EINVAL, "density must be in [0, 1]");
+    if (!(salt_ratio >= 0.0 && salt_ratio <= 1.0)) return fail(PHG_EINVAL, "salt_ratio must be in [0, 1]");
+    PHG_TRY(check_dims(img->width, img->rows));
+    if (density == 0.0) return PHG_OK;
+    phg::GenArgs a{};
+    a.img = img->data;
+    a.pitch = img->pitch;
+    a.image_stride = img->image_stride;
+    a.width = img->width;
+    a.rows = img->rows;
+    a.row_base = row_base;
+    a.height = height;
+    a.seed = seed;
+    a.all = density >= 1.0;
+    a.salt_all = salt_ratio >= 1.0;
+    a.thresh = a.all ? ~0ull : static_cast<uint64_t>(std::ldexp(density, 64));
+    a.salt_thresh = a.salt_all ? ~0ull : static_cast<uint64_t>(std::ldexp(salt_ratio, 64));
+    a.count = reinterpret_cast<unsigned long long*>(count);
+    if (img->n_images > 65535) return fail(PHG_EINVAL, "at most 65535 images per call");
+    a.n = img->n_images;
+    dim3 grid((img->width + 255) / 256, std::min(img->rows, 65535), img->n_images);
+    phg::gen_noise_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
+    ++g_launches;
+    PHG_CUDA(cudaGetLastError());
     return PHG_OK;
 }
 
