@@ -19,36 +19,6 @@
 #include "swar.cuh"
 
 // build-time switches for A/B experiments (defaults = product)
-#ifndef PHG_SCAN_BALLOT
-#define PHG_SCAN_BALLOT 0
-#endif
-#ifndef PHG_PROC_SWAR
-#define PHG_PROC_SWAR 0
-#endif
-#ifndef PHG_RMS_RSQ
-#define PHG_RMS_RSQ 0
-#endif
-#ifndef PHG_DBG_NO_REPL
-#define PHG_DBG_NO_REPL 0
-#endif
-#ifndef PHG_DBG_NO_PROCESS
-#define PHG_DBG_NO_PROCESS 0
-#endif
-#ifndef PHG_LIST_OFFCHAIN
-#define PHG_LIST_OFFCHAIN 1
-#endif
-#ifndef PHG_REPL_OWN
-#define PHG_REPL_OWN 0
-#endif
-#ifndef PHG_VSYM
-#define PHG_VSYM 1
-#endif
-#ifndef PHG_FMA_ADD
-#define PHG_FMA_ADD 1
-#endif
-#ifndef PHG_INTERIOR_TAG
-#define PHG_INTERIOR_TAG 0
-#endif
 
 namespace phg {
 
@@ -161,34 +131,7 @@ __device__ __forceinline__ void load_row(const uint8_t* rowp, uint32_t (&v)[2 * 
     v[BETA] = c;
 }
 
-// Number of similar in-bounds neighbours per byte lane (centre excluded).
 __device__ __forceinline__ uint32_t fma_add(uint32_t x, uint32_t one, uint32_t k);
-
-template <int BETA, bool ALE, bool ROWS_OK>
-__device__ __forceinline__ uint32_t count_similar(const uint32_t (&win)[2 * BETA + 1][2 * BETA + 1],
-                                                  const uint32_t (&colm)[2 * BETA + 1],
-                                                  const uint32_t (&rowm)[2 * BETA + 1],
-                                                  uint32_t k7, uint32_t one) {
-    const uint32_t p = win[BETA][BETA];
-    uint32_t cnt = 0;
-#pragma unroll
-    for (int i = 0; i < 2 * BETA + 1; ++i) {
-#pragma unroll
-        for (int j = 0; j < 2 * BETA + 1; ++j) {
-            if (i == BETA && j == BETA) continue;
-            const uint32_t valid = ROWS_OK ? colm[j] : (colm[j] & rowm[i]);
-#if PHG_FMA_ADD
-            // the carry-trick add on the FMA pipe (the ALU pipe is the bottleneck)
-            const uint32_t d = __vabsdiffu4(p, win[i][j]);
-            const uint32_t tt = fma_add(d & kLo7, one, k7);
-            cnt += (valid & ~(ALE ? (d | tt) : (d & tt))) >> 7;
-#else
-            cnt += sim_bits<ALE>(p, win[i][j], k7, valid) >> 7;
-#endif
-        }
-    }
-    return cnt;
-}
 
 // Vertical pair symmetry: the same-column pair (y, y+d) is tested once, at
 // row y ("down", returned) and reused as the "up" neighbour of row y+d.
@@ -200,40 +143,6 @@ __device__ __forceinline__ uint32_t count_similar_vs(const uint32_t (&win)[2 * B
                                                      const uint32_t (&rowm)[2 * BETA + 1], uint32_t k7,
                                                      uint32_t one, const uint32_t (&up)[BETA],
                                                      uint32_t (&down)[BETA]);
-
-// round(sqrt(S/f)) half away from zero, exact for S <= 2^24 / 4, f <= 2^10:
-// r ~ sqrt(4S/f) (few-ulp estimate); the answer floor((sqrt(4S/f)+1)/2)
-// only changes at odd r, so m = nearest(r) decides it except when m is odd,
-// where m^2 f <= 4S settles the tie exactly in integers.
-// XU-free variant for the hot path: float(S) by the 2^23 magic, 1/f from a
-// table, rsqrt by the integer bit trick + two Newton steps (rel. error
-// < 5e-6, i.e. |r - sqrt(4S/f)| < 3e-3 << 1/2), nearest-int by the 1.5*2^23
-// magic; the same exact odd-m integer tie check as rms_round32.  Requires
-// 4S < 2^23 (beta <= 2).
-__device__ __forceinline__ uint32_t rms_round_fast(uint32_t S, uint32_t f, float rcp_f) {
-    const float s4 = __int_as_float(0x4b000000 | (4u * S)) - 8388608.0f;  // exact: 4S < 2^23
-    const float x = fmaxf(s4 * rcp_f, 1e-20f);
-    float y = __int_as_float(0x5f3759df - (__float_as_int(x) >> 1));
-    const float h = 0.5f * x;
-    y = y * fmaf(-h * y, y, 1.5f);
-    y = y * fmaf(-h * y, y, 1.5f);
-    const float r = x * y;
-    const int m = __float_as_int(r + 12582912.0f) - 0x4b400000;  // round to nearest
-    if (m & 1) return (static_cast<uint32_t>(m * m) * f <= 4u * S) ? (m + 1) >> 1 : (m - 1) >> 1;
-    return static_cast<uint32_t>(m) >> 1;
-}
-
-// Same rule with a single MUFU.RSQ (relative error ~2^-22, so
-// |r - sqrt(4S/f)| < 3e-4 for 4S/f <= 2^18): float(S) by the 2^23 magic,
-// 1/f from a table, nearest-int by the 1.5*2^23 magic.  4S < 2^23.
-__device__ __forceinline__ uint32_t rms_round_rsq(uint32_t S, uint32_t f, float rcp_f) {
-    const float s4 = __int_as_float(0x4b000000 | (4u * S)) - 8388608.0f;
-    const float x = fmaxf(s4 * rcp_f, 1e-20f);
-    const float r = x * rsqrtf(x);
-    const int m = __float_as_int(r + 12582912.0f) - 0x4b400000;
-    if (m & 1) return (static_cast<uint32_t>(m * m) * f <= 4u * S) ? (m + 1) >> 1 : (m - 1) >> 1;
-    return static_cast<uint32_t>(m) >> 1;
-}
 
 __device__ __forceinline__ uint32_t rms_round32(uint32_t S, uint32_t f) {
     const float x = fmaxf(__fdividef(static_cast<float>(4u * S), static_cast<float>(f)), 1e-30f);
@@ -288,57 +197,6 @@ __device__ __forceinline__ uint32_t fma_add(uint32_t x, uint32_t one, uint32_t k
     return r;
 }
 
-// One beta=1 candidate pixel with byte-SIMD: the 3x3 window is gathered
-// as three aligned row words, the 8 neighbours packed into two words, and
-// the dissimilar count and sum of squares come from VABSDIFF4 + IDP.4A.
-// Semantics identical to process_pixel<1> (removal_rows, denoise.hpp:192-217):
-// cells outside the image are 0 in the tile; the in-bounds count corrects f.
-template <bool ALE>
-__device__ __forceinline__ uint32_t process_b1(int y, int px, uint32_t interior, const uint8_t* src, uint8_t* dst,
-                                               int gx0, int gy0, int own_y_lo, int own_y_hi, const TileArgs& a,
-                                               uint32_t one, const float* rcp) {
-    const int base = (px - 1) & ~3;
-    const int shb = ((px - 1) & 3) * 8;
-    const uint8_t* r0 = src + (y - 1) * kRP + base;
-    uint32_t R[3];
-#pragma unroll
-    for (int r = 0; r < 3; ++r) R[r] = __funnelshift_r(lds32(r0 + r * kRP), lds32(r0 + r * kRP + 4), shb);
-    uint32_t n1, n2, p4;
-    asm("prmt.b32 %0, %1, %2, 0x4210;" : "=r"(n1) : "r"(R[0]), "r"(R[1]));  // t0 t1 t2 m0
-    asm("prmt.b32 %0, %1, %2, 0x6542;" : "=r"(n2) : "r"(R[1]), "r"(R[2]));  // m2 b0 b1 b2
-    asm("prmt.b32 %0, %1, 0, 0x1111;" : "=r"(p4) : "r"(R[1]));              // centre x4
-    const uint32_t d1 = __vabsdiffu4(n1, p4), d2 = __vabsdiffu4(n2, p4);
-    const uint32_t t1 = fma_add(d1 & kLo7, one, a.k7), t2 = fma_add(d2 & kLo7, one, a.k7);
-    const uint32_t dis1 = (ALE ? (d1 | t1) : (d1 & t1)) & kHi;
-    const uint32_t dis2 = (ALE ? (d2 | t2) : (d2 & t2)) & kHi;
-    const uint32_t fc = __dp4a(dis2, 0x01010101u, __dp4a(dis1, 0x01010101u, 0u)) >> 7;
-    const uint32_t S = __dp4a(n2 & msb_to_bytes(dis2), n2, __dp4a(n1 & msb_to_bytes(dis1), n1, 0u));
-    const int gc = gx0 + px;
-    const bool own = y >= own_y_lo && y < own_y_hi && px >= kLeftPx && px < kLeftPx + kOutPx && gc < a.width;
-    if (interior) {  // window inside the image and replacement already decided by the sweep
-#if PHG_RMS_RSQ
-        dst[y * kRP + px] = static_cast<uint8_t>(rms_round_rsq(S, fc, rcp[fc]));
-#else
-        dst[y * kRP + px] = static_cast<uint8_t>(rms_round32(S, fc));
-#endif
-        return 0u;  // counted by the sweep
-    }
-    const int p = (R[1] >> 8) & 0xff;
-    const int gr = gy0 + y;
-    const int inb = (3 - (gr == 0) - (gr == a.height - 1)) * (3 - (gc == 0) - (gc == a.width - 1));
-    const int f = static_cast<int>(fc) - (p >= a.alpha ? 9 - inb : 0);
-    const int pix_count = a.faithful ? 9 : inb;
-    if (f > pix_count - 3 && f > 0) {
-#if PHG_RMS_RSQ
-        dst[y * kRP + px] = static_cast<uint8_t>(rms_round_rsq(S, static_cast<uint32_t>(f), rcp[f]));
-#else
-        dst[y * kRP + px] = static_cast<uint8_t>(rms_round32(S, static_cast<uint32_t>(f)));
-#endif
-        return own ? 1u : 0u;
-    }
-    return 0;
-}
-
 template <int BETA, bool ALE, bool ROWS_OK>
 __device__ __forceinline__ uint32_t count_similar_vs(const uint32_t (&win)[2 * BETA + 1][2 * BETA + 1],
                                                      const uint32_t (&colm)[2 * BETA + 1],
@@ -380,7 +238,6 @@ __global__ void __launch_bounds__(kThreads)
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint64_t bar;
     __shared__ unsigned int red[T][2];
-    __shared__ float rcp[32];  // 1/f for the RMS rule
 
     const int sh = a.th + 2 * HALO;
     uint8_t* buf[2] = {smem, smem + buf_bytes(sh)};
@@ -402,7 +259,6 @@ __global__ void __launch_bounds__(kThreads)
         tma_load_4d(buf[0], &src_map, 0, x0 / kChunk, y0, img, &bar);
     }
     if (threadIdx.x < 2 * T) red[threadIdx.x >> 1][threadIdx.x & 1] = 0;
-    if (threadIdx.x < 32) rcp[threadIdx.x] = threadIdx.x ? 1.0f / static_cast<float>(threadIdx.x) : 0.0f;
 
     const int w = kFirstWord + threadIdx.x % kCompWords;  // region word
     const int g = threadIdx.x / kCompWords;
@@ -461,11 +317,7 @@ __global__ void __launch_bounds__(kThreads)
         // rows with the whole window inside the image need no row masks
         const int yint_lo = min(max(ylo, BETA - gy0), yhi);
         const int yint_hi = max(min(yhi, a.height - BETA - gy0), yint_lo);
-        uint32_t fl_acc = 0, rp_acc = 0;  // per-lane counts (bytes; < 256 rows per thread)
-#if PHG_REPL_OWN
-        uint32_t cb0 = 0, cb1 = 0, cb2 = 0, cb3 = 0;  // candidate shift register
-#endif
-#if PHG_VSYM
+        uint32_t fl_acc = 0;  // per-lane flagged counts (bytes; < 256 rows per thread)
         // same-column pairs for the first rows: up[d-1] = (ylo-d, ylo);
         // pend[d-2][q] = (ylo+1+q-d, ylo+1+q) for rows ylo+1+q, q < d-1
         uint32_t up[BETA];
@@ -488,7 +340,6 @@ __global__ void __launch_bounds__(kThreads)
                     pend[d - 2][q] = colm[BETA] & rv(ylo + 1 + q) & rv(ylo + 1 + q - d) & ~(ALE ? (db | tb) : (db & tb));
                 }
         }
-#endif
         auto row = [&](int y, auto rows_ok_tag) {
             constexpr bool ROWS_OK = decltype(rows_ok_tag)::value;
             load_row<BETA>(colp + (y + BETA) * kRP, win[NB - 1]);
@@ -501,7 +352,6 @@ __global__ void __launch_bounds__(kThreads)
                 rowm[i] = ROWS_OK || (rr >= 0 && rr < a.height) ? 0xffffffffu : 0u;
             }
             if (!ROWS_OK) row_in = rowm[BETA] != 0;
-#if PHG_VSYM
             uint32_t down[BETA];
             const uint32_t cnt = count_similar_vs<BETA, ALE, ROWS_OK>(win, colm, rowm, a.k7, a.one, up, down);
             // rotate the pending same-column pairs: up[d-1] for row y+1
@@ -516,9 +366,6 @@ __global__ void __launch_bounds__(kThreads)
                 }
             }
             up[0] = down[0];
-#else
-            const uint32_t cnt = count_similar<BETA, ALE, ROWS_OK>(win, colm, rowm, a.k7, a.one);
-#endif
             const uint32_t card = cnt + 0x01010101u;
             if constexpr (CARD) {
                 if (y >= HALO && y < HALO + out_rows && own_word && row_in) {
@@ -540,30 +387,12 @@ __global__ void __launch_bounds__(kThreads)
                 // words defer the whole decision to the replacement pass.
                 const bool interior = ROWS_OK && !col_border;
                 const uint32_t cand = interior ? (flagged & lt_bits(card, rep4(125u))) : flagged;
-                constexpr bool kTag = PHG_INTERIOR_TAG;
                 // pixels outside the image are kept at 0 (see process_pixel)
                 *reinterpret_cast<uint32_t*>(dstb + y * kRP + 4 * w) =
                     win[BETA][BETA] & (row_in ? inimg_bytes : 0u);
                 // bits 7,15,23,31 -> nibble (no carries: the shifted copies never overlap)
-#if PHG_REPL_OWN
-                // this thread's own candidates: 4 bits per row pushed into a
-                // 128-bit shift register (rows per group <= 32)
-                {
-                    const uint32_t nib = (cand * 0x00204081u) >> 28;
-                    cb3 = __funnelshift_l(cb2, cb3, 4);
-                    cb2 = __funnelshift_l(cb1, cb2, 4);
-                    cb1 = __funnelshift_l(cb0, cb1, 4);
-                    cb0 = (cb0 << 4) | nib;
-                }
-#else
-                // + bit 4: the word's candidates are decided interior replacements
-                cmap[y * kCompWords + (w - kFirstWord)] =
-                    static_cast<uint8_t>(((cand * 0x00204081u) >> 28) | (kTag && interior ? 0x10u : 0u));
-#endif
-                if (y >= HALO && y < HALO + out_rows) {
-                    fl_acc += (flagged & own_col) >> 7;
-                    if (kTag && interior) rp_acc += (cand & own_col) >> 7;
-                }
+                cmap[y * kCompWords + (w - kFirstWord)] = static_cast<uint8_t>((cand * 0x00204081u) >> 28);
+                if (y >= HALO && y < HALO + out_rows) fl_acc += (flagged & own_col) >> 7;
             }
 #pragma unroll
             for (int i = 0; i < NB - 1; ++i)
@@ -576,34 +405,6 @@ __global__ void __launch_bounds__(kThreads)
         for (int y = yint_hi; y < yhi; ++y) row(y, std::false_type{});
         if constexpr (CARD) continue;  // T == 1: the map is written, nothing else
         nfl[t] += __dp4a(fl_acc, 0x01010101u, 0u);
-        nrp[t] += __dp4a(rp_acc, 0x01010101u, 0u);
-#if PHG_REPL_OWN
-        // replacement by the thread that swept the word: no compaction; the
-        // warp runs as long as its busiest lane (src is immutable and every
-        // candidate pixel belongs to exactly one thread, so no barrier is needed
-        // before the end of the step)
-        __syncwarp();
-        if (ylo < yhi) {
-            const int nrows = yhi - ylo;
-            uint32_t cbs[4] = {cb0, cb1, cb2, cb3};
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                uint32_t m = cbs[k];
-                while (m) {
-                    const uint32_t lb = m & (0u - m);
-                    m ^= lb;
-                    const int P = 32 * k + __popc(lb - 1u);  // bit position in the 128-bit register
-                    const int y = ylo + nrows - 1 - (P >> 2);
-                    const int px = 4 * w + (P & 3);
-                    if (BETA == 1 && PHG_PROC_SWAR)
-                        nrp[t] += process_b1<ALE>(y, px, 0u, src, dstb, x0, gy0, HALO, HALO + out_rows, a, a.one, rcp);
-                    else
-                        nrp[t] += process_pixel<BETA>(y, px, 0u, src, dstb, x0, gy0, HALO, HALO + out_rows, a);
-                }
-            }
-        }
-        __syncthreads();
-#else
         __syncthreads();
         // replacement pass.  Each warp takes rows rlo+warp, +kWarps, ...; a
         // row's candidates (16 px per lane) are compacted with one warp scan
@@ -617,10 +418,7 @@ __global__ void __launch_bounds__(kThreads)
             int pending = 0;  // warp-uniform: items waiting at list[0, pending)
             auto item_px = [&](uint32_t it, uint32_t& r) {
                 const int yy = it >> 10, px = it & 1023;
-                if (BETA == 1 && PHG_PROC_SWAR)
-                    r = process_b1<ALE>(yy, px, 0u, src, dstb, x0, gy0, HALO, HALO + out_rows, a, a.one, rcp);
-                else
-                    r = process_pixel<BETA>(yy, px, 0u, src, dstb, x0, gy0, HALO, HALO + out_rows, a);
+                r = process_pixel<BETA>(yy, px, 0u, src, dstb, x0, gy0, HALO, HALO + out_rows, a);
             };
             // process list[h, h+n), n <= 64: two independent items per lane
             auto drain = [&](int h, int n) {
@@ -637,9 +435,6 @@ __global__ void __launch_bounds__(kThreads)
                 }
                 nrp[t] += r0 + r1;
             };
-#if PHG_DBG_NO_REPL
-            if (true) {} else
-#endif
             for (int y = rlo + warp; y < rhi; y += kWarps) {
                 // this lane's 16 px (4 words x 4 lanes) as 16 contiguous bits
                 const uint32_t e = *reinterpret_cast<const uint32_t*>(cmap + y * kCompWords + 4 * lane) & 0x0f0f0f0fu;
@@ -664,10 +459,6 @@ __global__ void __launch_bounds__(kThreads)
                 }
                 pending += total;
                 __syncwarp();
-#if PHG_DBG_NO_PROCESS
-                pending = 0;
-                continue;
-#endif
                 int h = 0;
                 for (; pending - h >= 64; h += 64) drain(h, 64);
                 pending -= h;
@@ -683,7 +474,6 @@ __global__ void __launch_bounds__(kThreads)
             }
             if (pending > 0) drain(0, pending);
         }
-#endif
         __syncthreads();
     }
 

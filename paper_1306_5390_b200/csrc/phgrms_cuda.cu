@@ -22,7 +22,6 @@
 #include <vector>
 
 #include "../../include/phgrms_b200.h"
-#include "kernel_b1.cuh"
 #include "kernel_card.cuh"
 #include "kernel_gen.cuh"
 #include "kernel_h2.cuh"
@@ -129,35 +128,11 @@ FusedFn select_fused(int beta, int T, bool ale) {
 
 int max_fused(int beta) { return beta == 1 ? 5 : beta == 2 ? 4 : 0; }
 
-using B1Fn = void (*)(const CUtensorMap, const phg::TileArgs, const uint32_t);
-
-template <int T, bool A>
-B1Fn b1_ptr() {
-    return phg::fused_b1_kernel<T, A>;
-}
-
-B1Fn select_b1(int T, bool ale) {
-#define PHG_CASE(TT) \
-    if (T == TT) return ale ? b1_ptr<TT, true>() : b1_ptr<TT, false>();
-    PHG_CASE(1) PHG_CASE(2) PHG_CASE(3) PHG_CASE(4) PHG_CASE(5)
-#undef PHG_CASE
-    return nullptr;
-}
-
 // staged rows per tile for the generic kernel (tunable: PHG_ROWS)
 int generic_rows_target() {
     static const int v = [] {
         const char* e = getenv("PHG_ROWS");
         return e ? std::max(16, std::min(200, atoi(e))) : 56;
-    }();
-    return v;
-}
-
-// staged rows per tile for the beta=1 kernel (tunable: PHG_B1_ROWS)
-int b1_rows_target() {
-    static const int v = [] {
-        const char* e = getenv("PHG_B1_ROWS");
-        return e ? std::max(16, std::min(200, atoi(e))) : 58;
     }();
     return v;
 }
@@ -399,21 +374,18 @@ int launch_fused(const phg_dev_image& src, const phg_dev_image& dst, int row_bas
                  uint64_t* counters, int kcap, cudaStream_t stream) {
     if (use_h2(p, iters))
         return launch_h2(src, dst, row_base, height, own_lo, own_hi, p, it0, iters, counters, kcap, stream);
-    const bool b1 = p.beta == 1 && getenv("PHG_B1_SYM");  // opt-in: see DESIGN.md (slower on B200)
-    FusedFn fn = b1 ? nullptr : select_fused(p.beta, iters, p.alpha <= 128);
-    B1Fn fn1 = b1 ? select_b1(iters, p.alpha <= 128) : nullptr;
-    if (!fn && !fn1) return fail(PHG_EINVAL, "no fused kernel for this beta / iteration count");
+    FusedFn fn = select_fused(p.beta, iters, p.alpha <= 128);
+    if (!fn) return fail(PHG_EINVAL, "no fused kernel for this beta / iteration count");
     const int halo = p.beta * iters;
-    const Launch L = plan_rows(own_hi - own_lo, halo, b1 ? b1_rows_target() : generic_rows_target());
+    const Launch L = plan_rows(own_hi - own_lo, halo, generic_rows_target());
     const int sh = L.th + 2 * halo;
-    const size_t smem = b1 ? phg::b1_smem_bytes(sh) : phg::smem_bytes(sh);
-    if (sh > 256) return fail(PHG_EINVAL, "tile too tall");
-    if (!b1 && sh > 64) return fail(PHG_EINVAL, "tile too tall for the candidate register (<= 32 rows per group)");
+    const size_t smem = phg::smem_bytes(sh);
+    if (sh > 64) return fail(PHG_EINVAL, "tile too tall");
     CUtensorMap map;
     PHG_TRY(encode_map(&map, src, sh));
-    PHG_CUDA(cudaFuncSetAttribute(b1 ? reinterpret_cast<const void*>(fn1) : reinterpret_cast<const void*>(fn),
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    phg::TileArgs a;
+    PHG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    phg::TileArgs a{};
     a.dst = dst.data;
     a.pitch = dst.pitch;
     a.image_stride = dst.image_stride;
@@ -447,10 +419,7 @@ int launch_fused(const phg_dev_image& src, const phg_dev_image& dst, int row_bas
             a2.counters += static_cast<int64_t>(z0) * kcap * 2;
         }
         dim3 grid(tiles_x, L.tiles_y, nz);
-        if (b1)
-            fn1<<<grid, phg::kB1Threads, smem, stream>>>(m2, a2, 1u);
-        else
-            fn<<<grid, phg::kThreads, smem, stream>>>(m2, a2);
+        fn<<<grid, phg::kThreads, smem, stream>>>(m2, a2);
         ++g_launches;
         PHG_CUDA(cudaGetLastError());
     }
