@@ -80,6 +80,7 @@ def main():
         ctr = torch.zeros((n, 1, 2), dtype=torch.int64, device=dev)
         iz = dev_image(y, w, h, n)
         params = PhgParams(20, 1, 1, 3, 0)
+        params2 = PhgParams(20, 2, 1, 3, 0)
         px = n * w * h
         ops = {
             "cardinality": (5.0, lambda: check(L.phg_dev_cardinality(C.byref(ix), 20, 1, C.c_void_p(card.data_ptr()),
@@ -92,6 +93,9 @@ def main():
             "removal": (6.0, lambda: check(L.phg_dev_removal(C.byref(ix), C.c_void_p(card.data_ptr()), cpitch,
                                                              C.byref(params), C.byref(iz),
                                                              C.c_void_p(ctr.data_ptr()), sh))),
+            "removal_beta2": (6.0, lambda: check(L.phg_dev_removal(C.byref(ix), C.c_void_p(card.data_ptr()), cpitch,
+                                                                   C.byref(params2), C.byref(iz),
+                                                                   C.c_void_p(ctr.data_ptr()), sh))),
         }
         for name, (bpp, fn) in ops.items():
             ms = timed(fn)

@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(256) count_lt_kernel(const int32_t* card, int6
 }
 
 // ---------------------------------------------------------------------------
-// denoise_pass with a caller-supplied cardinality map, beta = 1
+// denoise_pass with a caller-supplied cardinality map, beta = 1 or 2
 // (removal_rows, denoise.hpp:171-223): flagged <=> map < thr (the map is
 // honoured as given, never recomputed); a flagged pixel's 3x3 window gives
 // the dissimilar count and sum of squares; replace if flag > pix_count - 3
@@ -300,16 +300,34 @@ constexpr int kRmTW = 256;          // tile width (px)
 constexpr int kRmTH = 16;           // tile height (rows)
 constexpr int kRmSP = kRmTW + 32;   // staged row pitch: 16-px aprons
 
-template <bool ALE, bool VEC>
-__global__ void __launch_bounds__(256) removal_b1_kernel(const RemovalArgs a) {
-    __shared__ __align__(16) uint8_t tile[(kRmTH + 2) * kRmSP];
+// dissimilar mask (bit 7 per byte) of four pixel pairs: |a - b| >= alpha
+template <bool ALE>
+__device__ __forceinline__ uint32_t dis4(uint32_t a, uint32_t b, uint32_t k7) {
+    const uint32_t d = __vabsdiffu4(a, b);
+    const uint32_t t = (d & kLo7) + k7;
+    return (ALE ? (d | t) : (d & t)) & kHi;
+}
+
+// Flag count and sum of squares of the dissimilar cells among 4 window bytes.
+template <bool ALE>
+__device__ __forceinline__ void acc_window_word(uint32_t w, uint32_t p4, uint32_t k7, int& fc, uint32_t& S) {
+    const uint32_t dis = dis4<ALE>(w, p4, k7);
+    fc += __popc(dis);
+    S = __dp4a(w & msb_to_bytes(dis), w, S);
+}
+
+template <bool ALE, bool VEC, int BETA = 1>
+__global__ void __launch_bounds__(256) removal_tile_kernel(const RemovalArgs a) {
+    static_assert(BETA == 1 || BETA == 2, "tiled removal covers beta 1 and 2");
+    constexpr int W2 = (2 * BETA + 1) * (2 * BETA + 1);
+    __shared__ __align__(16) uint8_t tile[(kRmTH + 2 * BETA) * kRmSP];
     const int img = blockIdx.z;
     const int x0 = blockIdx.x * kRmTW, y0 = blockIdx.y * kRmTH;
     const uint8_t* src = a.src + img * a.image_stride;
-    // stage rows y0-1 .. y0+kRmTH, columns x0-16 .. x0+kRmTW+16 (zeros outside)
-    for (int i = threadIdx.x; i < (kRmTH + 2) * (kRmSP / 16); i += 256) {
+    // stage rows y0-BETA .. y0+kRmTH+BETA-1, columns x0-16 .. x0+kRmTW+16 (zeros outside)
+    for (int i = threadIdx.x; i < (kRmTH + 2 * BETA) * (kRmSP / 16); i += 256) {
         const int r = i / (kRmSP / 16), ch = i - r * (kRmSP / 16);
-        const int gy = y0 - 1 + r, gx = x0 - 16 + 16 * ch;
+        const int gy = y0 - BETA + r, gx = x0 - 16 + 16 * ch;
         uint4 v = make_uint4(0, 0, 0, 0);
         if (gy >= 0 && gy < a.height && gx >= 0 && gx < a.width) {
             v = *reinterpret_cast<const uint4*>(src + gy * a.pitch + gx);
@@ -346,38 +364,60 @@ __global__ void __launch_bounds__(256) removal_b1_kernel(const RemovalArgs a) {
 #pragma unroll
                 for (int j = 0; j < 4; ++j) cv[j] = j < nvalid ? cp[j] : 0x7fffffff;
             }
-            const uint8_t* c0 = tile + (ly + 1) * kRmSP + 16 + 4 * wcol;  // this word, staged
+            const uint8_t* c0 = tile + (ly + BETA) * kRmSP + 16 + 4 * wcol;  // this word, staged
             uint32_t out = *reinterpret_cast<const uint32_t*>(c0);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 if (cv[j] >= a.thr) continue;
                 ++fl;
-                // 3x3 window of lane j: three funnel-shifted row words
-                uint32_t R[3];
+                int fc = 0;
+                uint32_t S = 0, p;
+                if (BETA == 1) {
+                    // 3x3 window of lane j: three funnel-shifted row words
+                    uint32_t R[3];
 #pragma unroll
-                for (int r = 0; r < 3; ++r) {
-                    const uint8_t* rp0 = c0 + (r - 1) * kRmSP;
-                    const uint32_t lo = *reinterpret_cast<const uint32_t*>(rp0 - 4);
-                    const uint32_t mid = *reinterpret_cast<const uint32_t*>(rp0);
-                    const uint32_t hi = *reinterpret_cast<const uint32_t*>(rp0 + 4);
-                    // bytes j-1, j, j+1 of the word at lane 0
-                    R[r] = j == 0 ? __funnelshift_l(lo, mid, 8) : __funnelshift_r(mid, hi, 8 * (j - 1));
+                    for (int r = 0; r < 3; ++r) {
+                        const uint8_t* rp0 = c0 + (r - 1) * kRmSP;
+                        const uint32_t lo = *reinterpret_cast<const uint32_t*>(rp0 - 4);
+                        const uint32_t mid = *reinterpret_cast<const uint32_t*>(rp0);
+                        const uint32_t hi = *reinterpret_cast<const uint32_t*>(rp0 + 4);
+                        // bytes j-1, j, j+1 of the word at lane 0
+                        R[r] = j == 0 ? __funnelshift_l(lo, mid, 8) : __funnelshift_r(mid, hi, 8 * (j - 1));
+                    }
+                    const uint32_t p4 = prmt(R[1], 0, 0x1111);
+                    acc_window_word<ALE>(prmt(R[0], R[1], 0x4210), p4, a.k7, fc, S);  // t0 t1 t2 m0
+                    acc_window_word<ALE>(prmt(R[1], R[2], 0x6542), p4, a.k7, fc, S);  // m2 b0 b1 b2
+                    p = (R[1] >> 8) & 0xff;
+                } else {
+                    // 5x5 window: per row, W = columns j-2..j+1 and X = column j+2
+                    uint32_t Wr[5], Xr[5];
+#pragma unroll
+                    for (int r = 0; r < 5; ++r) {
+                        const uint8_t* rp0 = c0 + (r - 2) * kRmSP;
+                        const uint32_t lo = *reinterpret_cast<const uint32_t*>(rp0 - 4);
+                        const uint32_t mid = *reinterpret_cast<const uint32_t*>(rp0);
+                        const uint32_t hi = *reinterpret_cast<const uint32_t*>(rp0 + 4);
+                        Wr[r] = j < 2 ? __funnelshift_l(lo, mid, 8 * (2 - j)) : __funnelshift_r(mid, hi, 8 * (j - 2));
+                        Xr[r] = j < 2 ? (mid >> (8 * (j + 2))) : (hi >> (8 * (j - 2)));  // byte 0 = column j+2
+                    }
+                    const uint32_t p4 = prmt(Wr[2], 0, 0x2222);
+                    acc_window_word<ALE>(Wr[0], p4, a.k7, fc, S);
+                    acc_window_word<ALE>(Wr[1], p4, a.k7, fc, S);
+                    acc_window_word<ALE>(Wr[3], p4, a.k7, fc, S);
+                    acc_window_word<ALE>(Wr[4], p4, a.k7, fc, S);
+                    // column j+2 of rows 0,1,3,4 and row 2 without its centre byte
+                    const uint32_t x01 = prmt(Xr[0], Xr[1], 0x0040), x34 = prmt(Xr[3], Xr[4], 0x0040);
+                    acc_window_word<ALE>(prmt(x01, x34, 0x5410), p4, a.k7, fc, S);
+                    acc_window_word<ALE>(prmt(Wr[2], Xr[2], 0x4310), p4, a.k7, fc, S);
+                    p = (Wr[2] >> 16) & 0xff;
                 }
-                const uint32_t n1 = prmt(R[0], R[1], 0x4210);  // t0 t1 t2 m0
-                const uint32_t n2 = prmt(R[1], R[2], 0x6542);  // m2 b0 b1 b2
-                const uint32_t p4 = prmt(R[1], 0, 0x1111);
-                const uint32_t d1 = __vabsdiffu4(n1, p4), d2 = __vabsdiffu4(n2, p4);
-                const uint32_t t1 = (d1 & kLo7) + a.k7, t2 = (d2 & kLo7) + a.k7;
-                const uint32_t dis1 = (ALE ? (d1 | t1) : (d1 & t1)) & kHi;
-                const uint32_t dis2 = (ALE ? (d2 | t2) : (d2 & t2)) & kHi;
-                const int fc = __popc(dis1 | (dis2 >> 1));
-                const uint32_t S = __dp4a(n2 & msb_to_bytes(dis2), n2, __dp4a(n1 & msb_to_bytes(dis1), n1, 0u));
-                const int p = (R[1] >> 8) & 0xff;
                 const int gxj = gx + j;
-                const int inb = (3 - (gy == 0) - (gy == a.height - 1)) * (3 - (gxj == 0) - (gxj == a.width - 1));
+                const int inr = min(gy + BETA, a.height - 1) - max(gy - BETA, 0) + 1;
+                const int inc = min(gxj + BETA, a.width - 1) - max(gxj - BETA, 0) + 1;
+                const int inb = inr * inc;
                 // cells outside the image are 0 in the tile: dissimilar exactly when p >= alpha
-                const int f = fc - (p >= a.alpha ? 9 - inb : 0);
-                const int pix_count = a.faithful ? 9 : inb;
+                const int f = fc - (static_cast<int>(p) >= a.alpha ? W2 - inb : 0);
+                const int pix_count = a.faithful ? W2 : inb;
                 if (f > pix_count - 3 && f > 0) {
                     const uint32_t v = rms_round32(S, static_cast<uint32_t>(f));
                     out = (out & ~(0xffu << (8 * j))) | (v << (8 * j));

@@ -877,8 +877,8 @@ int phg_dev_sse(const phg_dev_image* a, const phg_dev_image* b, uint64_t* sse, v
 int phg_dev_removal(const phg_dev_image* src, const int32_t* card, int64_t card_pitch, const phg_params* p,
                     const phg_dev_image* dst, uint64_t* counters, void* stream) {
     PHG_TRY(validate(p));
-    if (p->beta == 1 && !getenv("PHG_NO_H2")) {
-        // tiled byte-SIMD pass (kernel_card.cuh removal_b1_kernel)
+    if (p->beta <= 2 && !getenv("PHG_NO_TILED_REMOVAL")) {
+        // tiled byte-SIMD pass (kernel_card.cuh removal_tile_kernel)
         if ((reinterpret_cast<uintptr_t>(src->data) | reinterpret_cast<uintptr_t>(dst->data) | src->pitch |
              src->image_stride) & 15 || src->pitch != dst->pitch || src->image_stride != dst->image_stride)
             return fail(PHG_EINVAL, "device images must be 16-byte aligned with 16-byte pitches");
@@ -908,10 +908,17 @@ int phg_dev_removal(const phg_dev_image* src, const int32_t* card, int64_t card_
             if (a2.counters) a2.counters += static_cast<int64_t>(z0) * 2;
             dim3 grid((src->width + phg::kRmTW - 1) / phg::kRmTW, (src->rows + phg::kRmTH - 1) / phg::kRmTH,
                       std::min(65535, src->n_images - z0));
-            if (ale && vec) phg::removal_b1_kernel<true, true><<<grid, 256, 0, st>>>(a2);
-            else if (ale) phg::removal_b1_kernel<true, false><<<grid, 256, 0, st>>>(a2);
-            else if (vec) phg::removal_b1_kernel<false, true><<<grid, 256, 0, st>>>(a2);
-            else phg::removal_b1_kernel<false, false><<<grid, 256, 0, st>>>(a2);
+            if (p->beta == 1) {
+                if (ale && vec) phg::removal_tile_kernel<true, true, 1><<<grid, 256, 0, st>>>(a2);
+                else if (ale) phg::removal_tile_kernel<true, false, 1><<<grid, 256, 0, st>>>(a2);
+                else if (vec) phg::removal_tile_kernel<false, true, 1><<<grid, 256, 0, st>>>(a2);
+                else phg::removal_tile_kernel<false, false, 1><<<grid, 256, 0, st>>>(a2);
+            } else {
+                if (ale && vec) phg::removal_tile_kernel<true, true, 2><<<grid, 256, 0, st>>>(a2);
+                else if (ale) phg::removal_tile_kernel<true, false, 2><<<grid, 256, 0, st>>>(a2);
+                else if (vec) phg::removal_tile_kernel<false, true, 2><<<grid, 256, 0, st>>>(a2);
+                else phg::removal_tile_kernel<false, false, 2><<<grid, 256, 0, st>>>(a2);
+            }
             ++g_launches;
             PHG_CUDA(cudaGetLastError());
         }

@@ -99,20 +99,22 @@ def test_cardmap_p2_on_gpu():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("beta", [1, 2])
 @pytest.mark.parametrize("alpha", [1, 20, 200])
 @pytest.mark.parametrize("border", [0, 1])
-def test_denoise_pass_tiled_beta1_vs_oracle(alpha, border):
+def test_denoise_pass_tiled_vs_oracle(beta, alpha, border):
     # denoise_pass with a caller-supplied map (denoise.hpp:243-283) on the
-    # tiled beta=1 kernel: multi-tile shapes, the true map and arbitrary maps
-    rng = np.random.default_rng(alpha * 7 + border)
-    for w, h in ((700, 301), (257, 17), (1023, 64)):
+    # tiled kernel: multi-tile shapes, the true map and arbitrary maps
+    rng = np.random.default_rng(alpha * 7 + border + 100 * beta)
+    for w, h in ((700, 301), (257, 17), (1023, 64), (5, 3)):
         img = O.inject_sp_noise(O.synth_image(w, h, w + h), 0.3, 0.5, alpha)
         for kind in ("true", "random"):
-            card = O.cardinality(img, alpha, 1) if kind == "true" else rng.integers(0, 10, (h, w)).astype(np.int32)
-            for thr in (1, 3, 7):
-                p = P.DenoiseParams(alpha, 1, 1, thr, P.BorderMode(border))
+            card = O.cardinality(img, alpha, beta) if kind == "true" else \
+                rng.integers(0, 26, (h, w)).astype(np.int32)
+            for thr in (1, 3, 7, 30):
+                p = P.DenoiseParams(alpha, beta, 1, thr, P.BorderMode(border))
                 out, st = P.denoise_pass(G.from_array(img), P.CardinalityMap(w, h, card.reshape(-1)), p)
-                ref, f, r = O.removal_pass(img, card, alpha, 1, thr, border)
+                ref, f, r = O.removal_pass(img, card, alpha, beta, thr, border)
                 assert np.array_equal(out.pixels, ref), (w, h, kind, thr)
                 assert (st.flagged, st.replaced) == (f, r)
 
