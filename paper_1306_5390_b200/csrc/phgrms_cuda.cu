@@ -164,7 +164,7 @@ Launch plan_rows_h2(int own_rows, int halo, int rows_target, int n_images, int t
     const int th_max = std::max(1, rows_target - 2 * halo);
     Launch best = plan_rows(own_rows, halo, rows_target);
     double best_cost = 1e300;
-    for (int th = std::min(th_max, own_rows); th >= std::max(1, std::min(16, own_rows)); --th) {
+    for (int th = std::min(th_max, own_rows); th >= std::max(1, std::min(4, own_rows)); --th) {
         const int64_t tiles_y = (own_rows + th - 1) / th;
         const int64_t ctas = (static_cast<int64_t>(n_images) * tiles_x * tiles_y + 1) / 2;
         const int64_t waves = (ctas + slots - 1) / slots;
