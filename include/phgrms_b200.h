@@ -103,6 +103,19 @@ int phg_denoise(const uint8_t* img, int width, int height, const phg_params* p, 
 int phg_denoise_batch(const uint8_t* imgs, int n, int width, int height, const phg_params* p,
                       uint8_t* out, phg_pass_stats* stats, int* iterations_run);
 
+/* The Parallel engine (denoise.hpp:97-135) with GPUs as the workers, driven
+ * from one process: devices[0..ndev) are the workers of row_blocks
+ * (denoise.hpp:97-107).  n > 1 splits the batch into ndev image shards, one
+ * host thread per distinct device, no exchange; n == 1 splits the image into
+ * ndev row bands with a halo exchanged between devices after every fused
+ * launch (peer copies).  A device may appear more than once.  Same outputs
+ * and stats layout as phg_denoise_batch, bit-identical to phg_denoise.
+ * Errors: PHG_EINVAL "devices must list at least one GPU", "device D does
+ * not exist". */
+int phg_denoise_sharded(const uint8_t* imgs, int n, int width, int height, const phg_params* p,
+                        const int* devices, int ndev, uint8_t* out, phg_pass_stats* stats,
+                        int* iterations_run);
+
 /* Input generators restated from the reference (out of the hot path; used
  * to build bench inputs without the oracle): synth_image(SmoothRandom=2,
  * Gradient=0, Checker=1), image.hpp:53-106; inject_sp_noise, noise.hpp:62-89

@@ -21,6 +21,7 @@ from .phgrms import (  # noqa: F401
     compute_cardinality,
     denoise,
     denoise_batch,
+    denoise_sharded,
     denoise_pass,
     inject_sp_noise,
     format_db,

@@ -24,7 +24,7 @@ EXPORTS = (
     "phg_inject_sp_noise", "phg_max_fused_iterations", "phg_dev_fused_step",
     "phg_dev_denoise", "phg_dev_cardinality", "phg_dev_removal", "phg_finalize_stats",
     "phg_fused_kernel_name", "phg_residual_noise_count", "phg_sse", "phg_dev_residual_count", "phg_dev_sse",
-    "phg_dev_synth_smooth", "phg_dev_inject_noise",
+    "phg_dev_synth_smooth", "phg_dev_inject_noise", "phg_denoise_sharded",
 )
 
 
@@ -80,6 +80,9 @@ def lib():
                                   C.c_void_p, C.POINTER(PhgPassStats), C.POINTER(C.c_int)]
         L.phg_denoise_batch.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(PhgParams),
                                         C.c_void_p, C.POINTER(PhgPassStats), C.POINTER(C.c_int)]
+        L.phg_denoise_sharded.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(PhgParams),
+                                          C.POINTER(C.c_int), C.c_int, C.c_void_p, C.POINTER(PhgPassStats),
+                                          C.POINTER(C.c_int)]
         L.phg_synth_image.argtypes = [C.c_int, C.c_int, C.c_uint32, C.c_int, _u8p]
         L.phg_inject_sp_noise.argtypes = [_u8p, C.c_int, C.c_int, C.c_double, C.c_double, C.c_uint32,
                                           _u8p, C.c_void_p]

@@ -15,10 +15,12 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <deque>
 #include <mutex>
 #include <numeric>
 #include <random>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/phgrms_b200.h"
@@ -551,7 +553,7 @@ struct DeviceState {
 };
 
 std::mutex g_mu;
-std::vector<DeviceState> g_dev;
+std::deque<DeviceState> g_dev;  // deque: growing keeps references to existing states valid
 
 int current_state(DeviceState** out, int* dev_out = nullptr) {
     int dev = 0;
@@ -1327,3 +1329,202 @@ int64_t phg_inject_sp_noise(const uint8_t* img, int w, int h, double density, do
 }
 
 }  // extern "C"
+
+// ===================================================== multi-device shards
+// phg_denoise_sharded: the reference's Parallel engine (row_blocks over
+// workers, denoise.hpp:97-135) with GPUs as the workers, for a C/C++ caller
+// that has no torch.distributed.  The process drives every listed device
+// itself (the one-process-per-GPU form is paper_1306_5390_b200/dist.py).
+//   - a batch (n > 1) splits the images with the row_blocks formula, one
+//     shard per list entry; each device runs phg_denoise_batch on its shards
+//     from its own host thread.  No exchange.
+//   - one image splits into row bands, band g on devices[g], each held with
+//     a beta*Tmax halo; after every fused launch the halo rows are copied
+//     from the owning band (cudaMemcpyPeerAsync: NVLink on an NVSwitch node,
+//     a plain device copy when two bands share a device).
+// A device may be listed more than once; its shards then run in order on
+// that device.  Results are bit-identical to phg_denoise for every list.
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    DeviceGuard() { cudaGetDevice(&prev); }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+int check_devices(const int* devices, int ndev) {
+    if (!devices || ndev < 1) return fail(PHG_EINVAL, "devices must list at least one GPU");
+    int count = 0;
+    PHG_CUDA(cudaGetDeviceCount(&count));
+    for (int g = 0; g < ndev; ++g)
+        if (devices[g] < 0 || devices[g] >= count)
+            return fail(PHG_EINVAL, "device " + std::to_string(devices[g]) + " does not exist");
+    return PHG_OK;
+}
+
+struct ShardBand {
+    int dev;
+    DeviceState* s;
+    int lo, hi, blo, bhi;
+    phg_dev_image a, b;
+    cudaEvent_t done = nullptr;  // recorded after each fused launch
+    uint64_t* ctr;               // the device's counters [k][2]
+};
+
+int sharded_bands(const uint8_t* img, int w, int h, const phg_params& p, const int* devices, int ndev,
+                  uint8_t* out, phg_pass_stats* stats, int* iterations_run) {
+    const int k = p.max_iterations;
+    const std::vector<int> plan = chunk_plan(k, p.beta);
+    const int halo = p.beta * *std::max_element(plan.begin(), plan.end());
+    const int64_t pitch = round_up(w, 16);
+    std::vector<ShardBand> bands;
+    std::vector<int> devs;  // unique, in first-use order
+    std::vector<uint64_t*> dev_ctr;
+    struct Events {
+        std::vector<ShardBand>* b;
+        ~Events() {
+            for (auto& x : *b)
+                if (x.done) cudaEventDestroy(x.done);
+        }
+    } cleanup{&bands};
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int g = 0; g < ndev; ++g) {
+        const int lo = static_cast<int>(static_cast<int64_t>(h) * g / ndev);
+        const int hi = static_cast<int>(static_cast<int64_t>(h) * (g + 1) / ndev);
+        if (hi <= lo) continue;  // row_blocks skips empty blocks (denoise.hpp:104)
+        ShardBand b{};
+        b.dev = devices[g];
+        PHG_CUDA(cudaSetDevice(b.dev));
+        PHG_TRY(current_state(&b.s));
+        const size_t di = std::find(devs.begin(), devs.end(), b.dev) - devs.begin();
+        if (di == devs.size()) {
+            void* pk;
+            PHG_TRY(scratch(b.s, 5, sizeof(uint64_t) * 2 * k, &pk));
+            PHG_CUDA(cudaMemsetAsync(pk, 0, sizeof(uint64_t) * 2 * k, b.s->stream));
+            devs.push_back(b.dev);
+            dev_ctr.push_back(static_cast<uint64_t*>(pk));
+        }
+        b.ctr = dev_ctr[di];
+        b.lo = lo;
+        b.hi = hi;
+        b.blo = std::max(0, lo - halo);
+        b.bhi = std::min(h, hi + halo);
+        const int slot = 40 + 2 * g;
+        void *pa, *pb;
+        PHG_TRY(scratch(b.s, slot, static_cast<size_t>(pitch) * (b.bhi - b.blo), &pa));
+        PHG_TRY(scratch(b.s, slot + 1, static_cast<size_t>(pitch) * (b.bhi - b.blo), &pb));
+        b.a = make_image(pa, w, b.bhi - b.blo, 1);
+        b.b = make_image(pb, w, b.bhi - b.blo, 1);
+        PHG_CUDA(cudaEventCreateWithFlags(&b.done, cudaEventDisableTiming));
+        bands.push_back(b);
+        ShardBand& nb = bands.back();
+        PHG_CUDA(cudaMemcpy2DAsync(nb.a.data, pitch, img + static_cast<int64_t>(nb.blo) * w, w, w,
+                                   nb.bhi - nb.blo, cudaMemcpyHostToDevice, nb.s->stream));
+    }
+    int it0 = 0;
+    for (const int iters : plan) {
+        for (auto& b : bands) {
+            PHG_CUDA(cudaSetDevice(b.dev));
+            PHG_TRY(step(b.a, b.b, b.blo, h, b.lo, b.hi, p, it0, iters, b.ctr, k, b.s->stream));
+            PHG_CUDA(cudaEventRecord(b.done, b.s->stream));
+        }
+        // halo rows of band b from their owners.  Every owner o of a halo row
+        // of b also reads b's rows (the halo relation is symmetric), which
+        // orders b's copy before o's launch two chunks on (the WAR on o.b).
+        for (auto& b : bands) {
+            PHG_CUDA(cudaSetDevice(b.dev));
+            for (auto& o : bands) {
+                if (&o == &b) continue;
+                const int r0 = std::max(b.blo, o.lo), r1 = std::min(b.bhi, o.hi);
+                if (r1 <= r0) continue;
+                PHG_CUDA(cudaStreamWaitEvent(b.s->stream, o.done, 0));
+                PHG_CUDA(cudaMemcpyPeerAsync(b.b.data + (r0 - b.blo) * pitch, b.dev,
+                                             o.b.data + (r0 - o.blo) * pitch, o.dev, (r1 - r0) * pitch,
+                                             b.s->stream));
+            }
+        }
+        for (auto& b : bands) std::swap(b.a, b.b);
+        it0 += iters;
+    }
+    for (auto& b : bands) {
+        PHG_CUDA(cudaSetDevice(b.dev));
+        PHG_CUDA(cudaMemcpy2DAsync(out + static_cast<int64_t>(b.lo) * w, w,
+                                   b.a.data + static_cast<int64_t>(b.lo - b.blo) * pitch, pitch, w, b.hi - b.lo,
+                                   cudaMemcpyDeviceToHost, b.s->stream));
+    }
+    std::vector<uint64_t> total(2 * k, 0), part(2 * k);
+    for (size_t d = 0; d < devs.size(); ++d) {
+        PHG_CUDA(cudaSetDevice(devs[d]));
+        DeviceState* s;
+        PHG_TRY(current_state(&s));
+        PHG_CUDA(cudaMemcpyAsync(part.data(), dev_ctr[d], sizeof(uint64_t) * 2 * k, cudaMemcpyDeviceToHost,
+                                 s->stream));
+        PHG_CUDA(cudaStreamSynchronize(s->stream));
+        for (int i = 0; i < 2 * k; ++i) total[i] += part[i];
+    }
+    const float ms = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    return finalize(total, 1, k, ms, stats, iterations_run);
+}
+
+int sharded_batch(const uint8_t* imgs, int n, int w, int h, const phg_params* p, const int* devices, int ndev,
+                  uint8_t* out, phg_pass_stats* stats, int* iterations_run) {
+    const int k = p->max_iterations;
+    const int64_t img_bytes = static_cast<int64_t>(w) * h;
+    std::vector<int> devs;
+    for (int g = 0; g < ndev; ++g)
+        if (std::find(devs.begin(), devs.end(), devices[g]) == devs.end()) devs.push_back(devices[g]);
+    struct Result {
+        int rc = PHG_OK;
+        std::string err;
+        int64_t launches = 0;
+    };
+    std::vector<Result> res(devs.size());
+    auto work = [&](size_t d) {
+        Result& r = res[d];
+        const cudaError_t e = cudaSetDevice(devs[d]);
+        if (e != cudaSuccess) {
+            r.rc = PHG_ECUDA;
+            r.err = std::string("cudaSetDevice: ") + cudaGetErrorString(e);
+            return;
+        }
+        g_launches = 0;
+        for (int g = 0; g < ndev && r.rc == PHG_OK; ++g) {
+            if (devices[g] != devs[d]) continue;
+            const int i0 = static_cast<int>(static_cast<int64_t>(n) * g / ndev);
+            const int i1 = static_cast<int>(static_cast<int64_t>(n) * (g + 1) / ndev);
+            if (i1 <= i0) continue;
+            r.rc = phg_denoise_batch(imgs + img_bytes * i0, i1 - i0, w, h, p, out + img_bytes * i0,
+                                     stats + static_cast<int64_t>(k) * i0, iterations_run + i0);
+            if (r.rc != PHG_OK) r.err = g_error;
+        }
+        r.launches = g_launches;
+    };
+    std::vector<std::thread> pool;
+    for (size_t d = 1; d < devs.size(); ++d) pool.emplace_back(work, d);
+    const int64_t mine = g_launches;
+    work(0);
+    const int64_t here = res[0].launches;
+    for (auto& t : pool) t.join();
+    g_launches = mine + here;
+    for (size_t d = 1; d < devs.size(); ++d) g_launches += res[d].launches;
+    for (auto& r : res)
+        if (r.rc != PHG_OK) return fail(r.rc, r.err);
+    return PHG_OK;
+}
+
+}  // namespace
+
+extern "C" int phg_denoise_sharded(const uint8_t* imgs, int n, int w, int h, const phg_params* p,
+                                   const int* devices, int ndev, uint8_t* out, phg_pass_stats* stats,
+                                   int* iterations_run) {
+    PHG_TRY(validate(p));
+    PHG_TRY(check_dims(w, h));
+    if (n < 1) return fail(PHG_EINVAL, "batch must hold at least one image");
+    if (!devices || ndev < 1) return fail(PHG_EINVAL, "devices must list at least one GPU");
+    PHG_TRY(check_devices(devices, ndev));
+    DeviceGuard guard;
+    if (n > 1) return sharded_batch(imgs, n, w, h, p, devices, ndev, out, stats, iterations_run);
+    return sharded_bands(imgs, w, h, *p, devices, ndev, out, stats, iterations_run);
+}

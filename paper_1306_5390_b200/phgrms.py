@@ -300,6 +300,30 @@ def denoise_batch(imgs: np.ndarray, params: DenoiseParams):
     return out, per
 
 
+def denoise_sharded(imgs: np.ndarray, params: DenoiseParams, devices):
+    """The Parallel engine with GPUs as workers, from one process
+    (phg_denoise_sharded; denoise.hpp:97-135): ``imgs`` is uint8 [h, w] (one
+    image, row bands over ``devices`` with halo exchange) or [n, h, w] (image
+    shards).  Returns (images, per-image PassStats lists) like denoise_batch;
+    bit-identical to denoise() for every device list."""
+    params.validate()
+    imgs = np.ascontiguousarray(imgs, np.uint8)
+    single = imgs.ndim == 2
+    batch = imgs[None] if single else imgs
+    n, h, w = batch.shape
+    k = params.max_iterations
+    out = np.empty_like(batch)
+    stats = (PhgPassStats * (n * k))()
+    its = (C.c_int * n)()
+    devs = (C.c_int * max(1, len(devices)))(*[int(d) for d in devices])
+    p = params._c()
+    check(lib().phg_denoise_sharded(batch.ctypes.data, n, w, h, C.byref(p), devs, len(devices),
+                                    out.ctypes.data, stats, its))
+    per = [[PassStats(s.iteration, s.flagged, s.replaced, s.elapsed_ms) for s in stats[i * k: i * k + its[i]]]
+           for i in range(n)]
+    return (out[0], per[0]) if single else (out, per)
+
+
 def residual_noise_count(img: GrayImage, alpha: int, beta: int, card_threshold: int) -> int:
     """metrics.hpp:52-59 -- pixels whose cardinality is below the threshold
     (beta = 1: counted by the fp16 two-tile sweep, no map is written)."""

@@ -116,3 +116,21 @@ def test_compute_entry_points_fail_loudly_without_gpu():
         pass
     with pytest.raises(P.CudaError):
         P.compute_cardinality(P.GrayImage(4, 4, 1), 20, 1)
+
+
+def test_sharded_argument_errors_without_gpu():
+    # phg_denoise_sharded validates the parameters and the device list
+    # before touching CUDA; with no GPU the device check fails loudly
+    img = np.zeros((4, 4), np.uint8)
+    with pytest.raises(P.InvalidArgument, match="alpha must be in"):
+        P.denoise_sharded(img, P.DenoiseParams(alpha=0), [0])
+    with pytest.raises(P.InvalidArgument, match="devices must list at least one GPU"):
+        P.denoise_sharded(img, P.DenoiseParams(), [])
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return
+    except ImportError:
+        pass
+    with pytest.raises(P.CudaError):
+        P.denoise_sharded(img, P.DenoiseParams(), [0])
