@@ -76,6 +76,7 @@ struct H2Args {
     int it0;
     int kcap;
     unsigned long long* counters;  // [n_images][kcap][2]
+    HaloPeers peers;               // single-image bands only (kernels.cuh)
 };
 
 // ------------------------------------------------------------ fp16 helpers
@@ -522,12 +523,14 @@ __global__ void __launch_bounds__(kH2Threads, 2)
                 o.x = prmt(u0.x, u0.y, 0x6420); o.y = prmt(u0.z, u0.w, 0x6420);
                 o.z = prmt(u1.x, u1.y, 0x6420); o.w = prmt(u1.z, u1.w, 0x6420);
                 *reinterpret_cast<uint4*>(gA + static_cast<int64_t>(y) * a.pitch + 16 * ch) = o;
+                mirror_row16(a.peers, a.row_base + y0A + y, a.pitch, x0A + kLeftPx + 16 * ch, o);
             }
             if (r < outB && x0B + kLeftPx + 16 * ch < a.width) {
                 uint4 o;
                 o.x = prmt(u0.x, u0.y, 0x7531); o.y = prmt(u0.z, u0.w, 0x7531);
                 o.z = prmt(u1.x, u1.y, 0x7531); o.w = prmt(u1.z, u1.w, 0x7531);
                 *reinterpret_cast<uint4*>(gB + static_cast<int64_t>(y) * a.pitch + 16 * ch) = o;
+                mirror_row16(a.peers, a.row_base + y0B + y, a.pitch, x0B + kLeftPx + 16 * ch, o);
             }
         }
     }

@@ -54,6 +54,23 @@ __host__ __device__ constexpr int smem_bytes(int sh) {
     return 2 * buf_bytes(sh) + (kCompWords * sh + 127) / 128 * 128 + kWarps * kRing * 2;
 }
 
+// Halo mirrors for row-band sharding (phg_denoise_sharded): owned output
+// rows that lie in a neighbour band's halo are also stored into that band's
+// next buffer -- a peer pointer over NVLink when the band lives on another
+// device -- so no exchange step runs between launches.  Unused: lo == hi.
+struct HaloPeers {
+    uint8_t* ptr[2];  // peer band buffer, same pitch; buffer row 0 = global row row0[i]
+    int row0[2];
+    int lo[2], hi[2];  // global rows mirrored to peer i
+};
+
+__device__ __forceinline__ void mirror_row16(const HaloPeers& hp, int gy, int64_t pitch, int col, uint4 v) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+        if (gy >= hp.lo[i] && gy < hp.hi[i])
+            *reinterpret_cast<uint4*>(hp.ptr[i] + static_cast<int64_t>(gy - hp.row0[i]) * pitch + col) = v;
+}
+
 struct TileArgs {
     uint8_t* dst;
     int64_t pitch;
@@ -76,6 +93,7 @@ struct TileArgs {
     int32_t* card_out;             // CARD mode: [n][rows][card_pitch] (rows from row_base)
     int64_t card_pitch;            // elements
     int64_t card_stride;           // elements per image
+    HaloPeers peers;               // single-image bands only
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -489,6 +507,7 @@ __global__ void __launch_bounds__(kThreads)
             const int y = HALO + r;
             const uint4 v = *reinterpret_cast<const uint4*>(fin + y * kRP + kLeftPx + 16 * ch);
             *reinterpret_cast<uint4*>(gbase + static_cast<int64_t>(y) * a.pitch + 16 * ch) = v;
+            mirror_row16(a.peers, a.row_base + y0 + y, a.pitch, x0 + kLeftPx + 16 * ch, v);
         }
     }
 
@@ -533,6 +552,7 @@ struct ScalarArgs {
     int it0;
     int kcap;
     unsigned long long* counters;
+    HaloPeers peers;  // kModeFused on single-image bands
 };
 
 // One thread per pixel, global loads (L1/L2 serve the window re-reads).
@@ -585,6 +605,10 @@ __global__ void __launch_bounds__(256) scalar_kernel(const ScalarArgs a) {
                 }
             }
             a.dst[img * a.image_stride + yb * a.pitch + c] = static_cast<uint8_t>(out);
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+                if (gr >= a.peers.lo[i] && gr < a.peers.hi[i])
+                    a.peers.ptr[i][static_cast<int64_t>(gr - a.peers.row0[i]) * a.pitch + c] = static_cast<uint8_t>(out);
         }
     }
     if (MODE != kModeCard && a.counters) {

@@ -225,9 +225,11 @@ uint16_t half_bits(float f) {
     return static_cast<uint16_t>(sign | (static_cast<uint32_t>(e) << 10) | m);
 }
 
+const phg::HaloPeers kNoPeers{};
+
 int launch_h2(const phg_dev_image& src, const phg_dev_image& dst, int row_base, int height, int own_lo,
               int own_hi, const phg_params& p, int it0, int iters, uint64_t* counters, int kcap,
-              cudaStream_t stream) {
+              cudaStream_t stream, const phg::HaloPeers& peers = kNoPeers) {
     H2Fn fn = select_h2(iters, p.alpha <= 128);
     if (!fn) return fail(PHG_EINVAL, "no two-tile kernel for this iteration count");
     const int halo = iters;
@@ -263,6 +265,7 @@ int launch_h2(const phg_dev_image& src, const phg_dev_image& dst, int row_base, 
     a.it0 = it0;
     a.kcap = kcap;
     a.counters = reinterpret_cast<unsigned long long*>(counters);
+    a.peers = peers;
     const unsigned grid = static_cast<unsigned>((n_tiles + 1) / 2);
     fn<<<grid, phg::kH2Threads, smem, stream>>>(map, a);
     ++g_launches;
@@ -373,9 +376,10 @@ int launch_card_tb(const phg_dev_image& src, int alpha, int beta, int32_t* card,
 
 int launch_fused(const phg_dev_image& src, const phg_dev_image& dst, int row_base, int height,
                  int own_lo, int own_hi, const phg_params& p, int it0, int iters,
-                 uint64_t* counters, int kcap, cudaStream_t stream) {
+                 uint64_t* counters, int kcap, cudaStream_t stream, const phg::HaloPeers& peers = kNoPeers) {
     if (use_h2(p, iters))
-        return launch_h2(src, dst, row_base, height, own_lo, own_hi, p, it0, iters, counters, kcap, stream);
+        return launch_h2(src, dst, row_base, height, own_lo, own_hi, p, it0, iters, counters, kcap, stream,
+                         peers);
     FusedFn fn = select_fused(p.beta, iters, p.alpha <= 128);
     if (!fn) return fail(PHG_EINVAL, "no fused kernel for this beta / iteration count");
     const int halo = p.beta * iters;
@@ -406,6 +410,7 @@ int launch_fused(const phg_dev_image& src, const phg_dev_image& dst, int row_bas
     a.kcap = kcap;
     a.counters = reinterpret_cast<unsigned long long*>(counters);
     a.one = 1u;
+    a.peers = peers;
     const int tiles_x = (src.width + phg::kOutPx - 1) / phg::kOutPx;
     for (int z0 = 0; z0 < src.n_images; z0 += 65535) {
         const int nz = std::min(65535, src.n_images - z0);
@@ -431,7 +436,8 @@ int launch_fused(const phg_dev_image& src, const phg_dev_image& dst, int row_bas
 int launch_scalar(int mode, const phg_dev_image& src, const phg_dev_image* dst,
                   const int32_t* card_in, int32_t* card_out, int64_t card_pitch, int row_base,
                   int height, int own_lo, int own_hi, const phg_params& p, int it0,
-                  uint64_t* counters, int kcap, cudaStream_t stream) {
+                  uint64_t* counters, int kcap, cudaStream_t stream,
+                  const phg::HaloPeers& peers = kNoPeers) {
     phg::ScalarArgs a;
     a.src = src.data;
     a.dst = dst ? dst->data : nullptr;
@@ -452,6 +458,7 @@ int launch_scalar(int mode, const phg_dev_image& src, const phg_dev_image* dst,
     a.it0 = it0;
     a.kcap = kcap;
     a.counters = reinterpret_cast<unsigned long long*>(counters);
+    a.peers = peers;
     const int rows = own_hi - own_lo;
     for (int z0 = 0; z0 < src.n_images; z0 += 65535) {
         const int nz = std::min(65535, src.n_images - z0);
@@ -483,13 +490,13 @@ int launch_scalar(int mode, const phg_dev_image& src, const phg_dev_image* dst,
 // available, else one scalar fused launch per iteration (iters must be 1).
 int step(const phg_dev_image& src, const phg_dev_image& dst, int row_base, int height, int own_lo,
          int own_hi, const phg_params& p, int it0, int iters, uint64_t* counters, int kcap,
-         cudaStream_t stream) {
+         cudaStream_t stream, const phg::HaloPeers& peers = kNoPeers) {
     if (max_fused(p.beta) > 0)
         return launch_fused(src, dst, row_base, height, own_lo, own_hi, p, it0, iters, counters,
-                            kcap, stream);
+                            kcap, stream, peers);
     if (iters != 1) return fail(PHG_EINVAL, "beta >= 3 runs one iteration per launch");
     return launch_scalar(phg::kModeFused, src, &dst, nullptr, nullptr, 0, row_base, height, own_lo,
-                         own_hi, p, it0, counters, kcap, stream);
+                         own_hi, p, it0, counters, kcap, stream, peers);
 }
 
 // Split k iterations into launches of at most max_fused(beta), evenly.
@@ -1339,9 +1346,15 @@ int64_t phg_inject_sp_noise(const uint8_t* img, int w, int h, double density, do
 //     shard per list entry; each device runs phg_denoise_batch on its shards
 //     from its own host thread.  No exchange.
 //   - one image splits into row bands, band g on devices[g], each held with
-//     a beta*Tmax halo; after every fused launch the halo rows are copied
-//     from the owning band (cudaMemcpyPeerAsync: NVLink on an NVSwitch node,
-//     a plain device copy when two bands share a device).
+//     a beta*Tmax halo.  When every band is at least a halo tall (its halo
+//     then belongs to its two neighbours alone) the fused kernels themselves
+//     store the owned rows that lie in a neighbour's halo into that
+//     neighbour's next buffer (HaloPeers, kernels.cuh): peer stores over
+//     NVLink, overlapped with the launch, and no exchange step.  The only
+//     synchronisation is event waits: launch c of a band follows launch c-1
+//     of both neighbours.  Thinner bands (or devices without peer access)
+//     copy halo rows from their owners after every launch
+//     (cudaMemcpyPeerAsync).
 // A device may be listed more than once; its shards then run in order on
 // that device.  Results are bit-identical to phg_denoise for every list.
 namespace {
@@ -1369,7 +1382,7 @@ struct ShardBand {
     DeviceState* s;
     int lo, hi, blo, bhi;
     phg_dev_image a, b;
-    cudaEvent_t done = nullptr;  // recorded after each fused launch
+    cudaEvent_t done[2] = {nullptr, nullptr};  // after fused launch c: done[c & 1]
     uint64_t* ctr;               // the device's counters [k][2]
 };
 
@@ -1386,7 +1399,8 @@ int sharded_bands(const uint8_t* img, int w, int h, const phg_params& p, const i
         std::vector<ShardBand>* b;
         ~Events() {
             for (auto& x : *b)
-                if (x.done) cudaEventDestroy(x.done);
+                for (auto e : x.done)
+                    if (e) cudaEventDestroy(e);
         }
     } cleanup{&bands};
     const auto t0 = std::chrono::steady_clock::now();
@@ -1417,18 +1431,71 @@ int sharded_bands(const uint8_t* img, int w, int h, const phg_params& p, const i
         PHG_TRY(scratch(b.s, slot + 1, static_cast<size_t>(pitch) * (b.bhi - b.blo), &pb));
         b.a = make_image(pa, w, b.bhi - b.blo, 1);
         b.b = make_image(pb, w, b.bhi - b.blo, 1);
-        PHG_CUDA(cudaEventCreateWithFlags(&b.done, cudaEventDisableTiming));
         bands.push_back(b);
+        for (auto& e : bands.back().done) PHG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         ShardBand& nb = bands.back();
         PHG_CUDA(cudaMemcpy2DAsync(nb.a.data, pitch, img + static_cast<int64_t>(nb.blo) * w, w, w,
                                    nb.bhi - nb.blo, cudaMemcpyHostToDevice, nb.s->stream));
     }
+    const int nb = static_cast<int>(bands.size());
+    bool peer = !getenv("PHG_SHARD_COPY");
+    for (int g = 0; g < nb; ++g) peer = peer && (nb == 1 || bands[g].hi - bands[g].lo >= halo);
+    for (int g = 0; peer && g + 1 < nb; ++g) {
+        const int d0 = bands[g].dev, d1 = bands[g + 1].dev;
+        if (d0 == d1) continue;
+        int ok01 = 0, ok10 = 0;
+        PHG_CUDA(cudaDeviceCanAccessPeer(&ok01, d0, d1));
+        PHG_CUDA(cudaDeviceCanAccessPeer(&ok10, d1, d0));
+        if (!ok01 || !ok10) {
+            peer = false;
+            break;
+        }
+        for (const auto& pr : {std::make_pair(d0, d1), std::make_pair(d1, d0)}) {
+            PHG_CUDA(cudaSetDevice(pr.first));
+            const cudaError_t e = cudaDeviceEnablePeerAccess(pr.second, 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled) {
+                cudaGetLastError();
+            } else {
+                PHG_CUDA(e);
+            }
+        }
+    }
     int it0 = 0;
-    for (const int iters : plan) {
+    if (peer) {
+        for (size_t c = 0; c < plan.size(); ++c) {
+            for (int g = 0; g < nb; ++g) {
+                ShardBand& b = bands[g];
+                PHG_CUDA(cudaSetDevice(b.dev));
+                phg::HaloPeers hp{};
+                if (g > 0) {  // rows of b in the upper neighbour's lower halo
+                    const ShardBand& u = bands[g - 1];
+                    if (c > 0) PHG_CUDA(cudaStreamWaitEvent(b.s->stream, u.done[(c - 1) & 1], 0));
+                    hp.ptr[0] = u.b.data;
+                    hp.row0[0] = u.blo;
+                    hp.lo[0] = b.lo;
+                    hp.hi[0] = std::min(b.hi, u.bhi);
+                }
+                if (g + 1 < nb) {  // rows of b in the lower neighbour's upper halo
+                    const ShardBand& d = bands[g + 1];
+                    if (c > 0) PHG_CUDA(cudaStreamWaitEvent(b.s->stream, d.done[(c - 1) & 1], 0));
+                    hp.ptr[1] = d.b.data;
+                    hp.row0[1] = d.blo;
+                    hp.lo[1] = std::max(b.lo, d.blo);
+                    hp.hi[1] = b.hi;
+                }
+                PHG_TRY(step(b.a, b.b, b.blo, h, b.lo, b.hi, p, it0, plan[c], b.ctr, k, b.s->stream, hp));
+                PHG_CUDA(cudaEventRecord(b.done[c & 1], b.s->stream));
+            }
+            for (auto& b : bands) std::swap(b.a, b.b);
+            it0 += plan[c];
+        }
+    }
+    for (size_t c = 0; !peer && c < plan.size(); ++c) {
+        const int iters = plan[c];
         for (auto& b : bands) {
             PHG_CUDA(cudaSetDevice(b.dev));
             PHG_TRY(step(b.a, b.b, b.blo, h, b.lo, b.hi, p, it0, iters, b.ctr, k, b.s->stream));
-            PHG_CUDA(cudaEventRecord(b.done, b.s->stream));
+            PHG_CUDA(cudaEventRecord(b.done[0], b.s->stream));
         }
         // halo rows of band b from their owners.  Every owner o of a halo row
         // of b also reads b's rows (the halo relation is symmetric), which
@@ -1439,7 +1506,7 @@ int sharded_bands(const uint8_t* img, int w, int h, const phg_params& p, const i
                 if (&o == &b) continue;
                 const int r0 = std::max(b.blo, o.lo), r1 = std::min(b.bhi, o.hi);
                 if (r1 <= r0) continue;
-                PHG_CUDA(cudaStreamWaitEvent(b.s->stream, o.done, 0));
+                PHG_CUDA(cudaStreamWaitEvent(b.s->stream, o.done[0], 0));
                 PHG_CUDA(cudaMemcpyPeerAsync(b.b.data + (r0 - b.blo) * pitch, b.dev,
                                              o.b.data + (r0 - o.blo) * pitch, o.dev, (r1 - r0) * pitch,
                                              b.s->stream));

@@ -49,3 +49,18 @@ def test_batch_shards_equal_per_image(n, ndev):
 def test_bad_device_rejected():
     with pytest.raises(P.InvalidArgument, match="does not exist"):
         P.denoise_sharded(np.zeros((8, 8), np.uint8), P.DenoiseParams(), [0, 4096])
+
+
+@pytest.mark.parametrize("ndev,beta,k", [(3, 1, 5), (4, 2, 9), (2, 3, 2)])
+def test_copy_exchange_equals_peer_stores(monkeypatch, ndev, beta, k):
+    # bands >= one halo tall use the kernels' peer stores; PHG_SHARD_COPY=1
+    # forces the copy exchange on the same split -- both equal the oracle
+    img = O.inject_sp_noise(O.synth_image(600, 211, 77 + beta), 0.25, 0.5, 3)
+    params = P.DenoiseParams(20, beta, k, 3)
+    ref, ref_stats = O.denoise(img, 20, beta, k, 3, 0)
+    peer, st_peer = P.denoise_sharded(img, params, [0] * ndev)
+    monkeypatch.setenv("PHG_SHARD_COPY", "1")
+    copy, st_copy = P.denoise_sharded(img, params, [0] * ndev)
+    assert np.array_equal(peer, ref) and np.array_equal(copy, ref)
+    assert [(s.flagged, s.replaced) for s in st_peer] == ref_stats
+    assert [(s.flagged, s.replaced) for s in st_copy] == ref_stats
