@@ -12,12 +12,16 @@
 // whole image as one device pipeline; Parallel(W) splits the rows into the
 // same row_blocks bands the reference hands to W threads, and the bands run
 // as separate device buffers with halo exchange -- bit-identical either way.
+// With PHGRMS_DEVICES set (e.g. "0,1,2,3"), Parallel(W)'s W bands are spread
+// over those GPUs in contiguous groups (phg_denoise_sharded): the
+// reference's own call scales across an NVSwitch node unchanged.
 // row_blocks / parallel_for_rows / similar / detail::rms_replacement remain
 // host utilities with the reference's contracts.
 
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <exception>
 #include <stdexcept>
 #include <string>
@@ -127,6 +131,21 @@ inline std::uint8_t rms_replacement(std::uint64_t sum_sq, int flag) {
     return static_cast<std::uint8_t>(std::min<std::uint64_t>(u, 255));
 }
 
+// PHGRMS_DEVICES: comma-separated device ordinals; empty when unset.
+inline std::vector<int> engine_devices() {
+    std::vector<int> d;
+    const char* e = std::getenv("PHGRMS_DEVICES");
+    if (!e) return d;
+    const std::string s(e);
+    std::size_t i = 0;
+    while (i < s.size()) {
+        const std::size_t j = std::min(s.find(',', i), s.size());
+        if (j > i) d.push_back(std::stoi(s.substr(i, j - i)));
+        i = j + 1;
+    }
+    return d;
+}
+
 inline void throw_on(int rc) {
     if (rc == PHG_OK) return;
     if (rc == PHG_EINVAL) throw std::invalid_argument(phg_last_error());
@@ -167,8 +186,18 @@ inline DenoiseResult denoise(const GrayImage& img, const DenoiseParams& params,
     std::vector<phg_pass_stats> st(static_cast<std::size_t>(params.max_iterations));
     int iters = 0;
     DenoiseResult r{GrayImage(img.width, img.height), {}};
-    detail::throw_on(phg_denoise(img.pixels.data(), img.width, img.height, &p, engine.resolved_workers(),
-                                 r.image.pixels.data(), st.data(), &iters));
+    const int workers = engine.resolved_workers();
+    const std::vector<int> devs = engine.mode == EngineMode::Parallel ? detail::engine_devices() : std::vector<int>{};
+    if (!devs.empty()) {
+        std::vector<int> band_dev(static_cast<std::size_t>(workers));
+        for (int g = 0; g < workers; ++g)
+            band_dev[g] = devs[static_cast<std::size_t>(static_cast<std::int64_t>(g) * devs.size() / workers)];
+        detail::throw_on(phg_denoise_sharded(img.pixels.data(), 1, img.width, img.height, &p, band_dev.data(),
+                                             workers, r.image.pixels.data(), st.data(), &iters));
+    } else {
+        detail::throw_on(phg_denoise(img.pixels.data(), img.width, img.height, &p, workers, r.image.pixels.data(),
+                                     st.data(), &iters));
+    }
     for (int i = 0; i < iters; ++i) r.stats.push_back({st[i].iteration, st[i].flagged, st[i].replaced, st[i].elapsed_ms});
     return r;
 }

@@ -134,6 +134,26 @@ int main(int argc, char** argv) {
             }
         }
     }
+    {  // PHGRMS_DEVICES: Parallel(W) bands spread over GPUs (device 0 listed twice)
+        setenv("PHGRMS_DEVICES", "0,0", 1);
+        std::mt19937 rng(202);
+        for (int i = 0; i < 10; ++i) {
+            const GrayImage img = random_image(rng, 16 + static_cast<int>(rng() % 600), 8 + static_cast<int>(rng() % 300));
+            DenoiseParams p;
+            p.beta = 1 + static_cast<int>(rng() % 2);
+            p.max_iterations = 1 + static_cast<int>(rng() % 9);
+            const auto serial = denoise(img, p, EngineSpec::serial());
+            for (const int w : {2, 5}) {
+                const auto par = denoise(img, p, EngineSpec::parallel(w));
+                CHECK(par.image == serial.image);
+                CHECK(par.stats.size() == serial.stats.size());
+                for (std::size_t s = 0; s < par.stats.size() && s < serial.stats.size(); ++s)
+                    CHECK(par.stats[s].flagged == serial.stats[s].flagged &&
+                          par.stats[s].replaced == serial.stats[s].replaced);
+            }
+        }
+        unsetenv("PHGRMS_DEVICES");
+    }
     {  // a zero-replacement pass is a fixed point
         std::mt19937 rng(106);
         for (int i = 0; i < 10; ++i) {
