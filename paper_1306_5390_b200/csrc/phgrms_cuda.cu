@@ -15,7 +15,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
-#include <deque>
+#include <memory>
 #include <mutex>
 #include <numeric>
 #include <random>
@@ -550,35 +550,65 @@ int launch_pitch(const uint8_t* src, uint8_t* dst, int w, int64_t pitch, int64_t
 // ------------------------------------------------------- per-device state
 constexpr int kMaxRowChunks = 16;
 
+// One state per (calling thread, device): streams, events and grow-only
+// scratch buffers.  Per thread, so that concurrent callers never share a
+// buffer or a stream -- the reference's functions are pure and "safe for
+// concurrent callers" -- and concurrent calls on one device
+// overlap on the GPU.  Freed when the thread exits.
 struct DeviceState {
+    int dev = -1;
     cudaStream_t stream = nullptr;
     cudaStream_t pipe[3] = {nullptr, nullptr, nullptr};  // chunked host<->device pipeline
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaEvent_t pev[3] = {nullptr, nullptr, nullptr};
     cudaEvent_t rin[kMaxRowChunks] = {}, rcomp[kMaxRowChunks] = {};  // single-image row pipeline
     std::vector<std::pair<void*, size_t>> bufs;  // grow-only scratch slots
+
+    DeviceState() = default;
+    DeviceState(const DeviceState&) = delete;
+    DeviceState& operator=(const DeviceState&) = delete;
+    ~DeviceState() {
+        if (dev < 0) return;
+        int prev = -1;
+        if (cudaGetDevice(&prev) != cudaSuccess) return;  // runtime already torn down
+        cudaSetDevice(dev);
+        if (stream) cudaStreamSynchronize(stream);
+        for (auto* p : pipe)
+            if (p) cudaStreamSynchronize(p);
+        for (auto& b : bufs)
+            if (b.first) cudaFree(b.first);
+        for (auto* e : {ev0, ev1}) if (e) cudaEventDestroy(e);
+        for (auto* e : pev) if (e) cudaEventDestroy(e);
+        for (int i = 0; i < kMaxRowChunks; ++i) {
+            if (rin[i]) cudaEventDestroy(rin[i]);
+            if (rcomp[i]) cudaEventDestroy(rcomp[i]);
+        }
+        for (auto* p : pipe) if (p) cudaStreamDestroy(p);
+        if (stream) cudaStreamDestroy(stream);
+        cudaSetDevice(prev);
+    }
 };
 
-std::mutex g_mu;
-std::deque<DeviceState> g_dev;  // deque: growing keeps references to existing states valid
+thread_local std::vector<std::unique_ptr<DeviceState>> g_dev;
 
 int current_state(DeviceState** out, int* dev_out = nullptr) {
     int dev = 0;
     PHG_CUDA(cudaGetDevice(&dev));
-    std::lock_guard<std::mutex> lk(g_mu);
     if (static_cast<int>(g_dev.size()) <= dev) g_dev.resize(dev + 1);
-    DeviceState& s = g_dev[dev];
+    if (!g_dev[dev]) g_dev[dev] = std::make_unique<DeviceState>();
+    DeviceState& s = *g_dev[dev];
     if (!s.stream) {
+        s.dev = dev;
         PHG_CUDA(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
         PHG_CUDA(cudaEventCreate(&s.ev0));
         PHG_CUDA(cudaEventCreate(&s.ev1));
         for (int i = 0; i < 3; ++i) {
             PHG_CUDA(cudaStreamCreateWithFlags(&s.pipe[i], cudaStreamNonBlocking));
             PHG_CUDA(cudaEventCreateWithFlags(&s.pev[i], cudaEventDisableTiming));
+        }
         for (int i = 0; i < kMaxRowChunks; ++i) {
             PHG_CUDA(cudaEventCreateWithFlags(&s.rin[i], cudaEventDisableTiming));
             PHG_CUDA(cudaEventCreateWithFlags(&s.rcomp[i], cudaEventDisableTiming));
-        }
         }
     }
     *out = &s;
@@ -849,20 +879,23 @@ int phg_dev_residual_count(const phg_dev_image* src, int alpha, int beta, int ca
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (beta == 1 && !getenv("PHG_NO_H2"))
         return launch_card_h2(*src, alpha, phg::kCardCount, card_threshold, nullptr, 0, counts, st);
-    // wider windows: scalar map into scratch, then count
-    DeviceState* s;
-    PHG_TRY(current_state(&s));
-    void* pc;
+    // wider windows: scalar map into a stream-ordered temporary, then count
+    void* pc = nullptr;
     const int64_t cpitch = round_up(src->width, 4);
-    PHG_TRY(scratch(s, 5, sizeof(int32_t) * cpitch * src->rows * src->n_images, &pc));
-    PHG_TRY(phg_dev_cardinality(src, alpha, beta, static_cast<int32_t*>(pc), cpitch, stream));
-    dim3 grid(std::max(1, std::min(1184, static_cast<int>((static_cast<int64_t>(src->width) * src->rows + 255) / 256))),
-              src->n_images);
-    phg::count_lt_kernel<<<grid, 256, 0, st>>>(static_cast<int32_t*>(pc), cpitch, src->width, src->rows,
-                                               src->n_images, card_threshold,
-                                               reinterpret_cast<unsigned long long*>(counts));
-    ++g_launches;
-    PHG_CUDA(cudaGetLastError());
+    PHG_CUDA(cudaMallocAsync(&pc, sizeof(int32_t) * cpitch * src->rows * src->n_images, st));
+    const int rc = phg_dev_cardinality(src, alpha, beta, static_cast<int32_t*>(pc), cpitch, stream);
+    if (rc == PHG_OK) {
+        dim3 grid(std::max(1, std::min(1184, static_cast<int>((static_cast<int64_t>(src->width) * src->rows + 255) / 256))),
+                  src->n_images);
+        phg::count_lt_kernel<<<grid, 256, 0, st>>>(static_cast<int32_t*>(pc), cpitch, src->width, src->rows,
+                                                   src->n_images, card_threshold,
+                                                   reinterpret_cast<unsigned long long*>(counts));
+        ++g_launches;
+    }
+    const cudaError_t le = cudaGetLastError();
+    PHG_CUDA(cudaFreeAsync(pc, st));
+    if (rc != PHG_OK) return rc;
+    PHG_CUDA(le);
     return PHG_OK;
 }
 
