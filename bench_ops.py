@@ -11,6 +11,9 @@ launching stream after warm-up; one JSON line per op.
                 algorithmic bytes 2 B in per pixel
   removal       phg_dev_removal (denoise_pass with a caller-supplied int32
                 map, denoise.hpp:243-283): 1 B image + 4 B map in, 1 B out
+  denoise_beta3 phg_dev_denoise, beta = 3 (7x7 windows), k = 4, on a 30%
+                salt-and-pepper image (device generators): 2 B per
+                pixel-iteration; the Mpixel_per_s column is pixel-iterations
 
 Workloads: the c4 batch (4096 x 481x321 = 632 Mpx) and one 16384^2 image
 (268 Mpx), both larger than L2.  Synthetic inputs (uniform random bytes):
@@ -34,6 +37,7 @@ sys.path.insert(0, ROOT)
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--only", default="", help="comma-separated op names")
     a = ap.parse_args()
     import torch
 
@@ -97,13 +101,29 @@ def main():
                                                                    C.byref(params2), C.byref(iz),
                                                                    C.c_void_p(ctr.data_ptr()), sh))),
         }
+        # beta = 3 denoise: clean smooth field + 30% noise (phg_dev_synth_smooth / inject)
+        k3 = 4
+        nz = torch.empty_like(x)
+        inz = dev_image(nz, w, h, n)
+        check(L.phg_dev_synth_smooth(C.byref(inz), 0, h, C.c_uint64(7), sh))
+        check(L.phg_dev_inject_noise(C.byref(inz), 0, h, C.c_double(0.3), C.c_double(0.5), C.c_uint64(9), None, sh))
+        ctr3 = torch.zeros((n, k3, 2), dtype=torch.int64, device=dev)
+        p3 = PhgParams(20, 3, k3, 3, 0)
+        ops["denoise_beta3"] = (2.0 * k3, lambda: check(L.phg_dev_denoise(C.byref(inz), C.byref(iy), C.byref(ix),
+                                                                          C.byref(p3), C.c_void_p(ctr3.data_ptr()),
+                                                                          sh)))
         for name, (bpp, fn) in ops.items():
+            if a.only and name not in a.only.split(","):
+                continue
             ms = timed(fn)
             gbs = px * bpp / (ms / 1e3) / 1e9
-            print(json.dumps({"op": name, "workload": wl, "ms": round(ms, 4), "Mpixel_per_s": round(px / ms / 1e3, 1),
+            units = px * (bpp / 2.0 if name.startswith("denoise") else 1.0)
+            print(json.dumps({"op": name, "workload": wl, "ms": round(ms, 4), "Mpixel_per_s": round(units / ms / 1e3, 1),
                               "alg_bytes_per_px": bpp, "achieved_GBs": round(gbs, 1), "peak_GBs": peak,
-                              "frac": round(gbs / peak, 4), "peak_source": peak_src, "data": "synthetic uniform"}))
-        del x, y, card
+                              "frac": round(gbs / peak, 4), "peak_source": peak_src,
+                              "data": ("device smooth field + 30% s&p" if name.startswith("denoise")
+                                       else "synthetic uniform")}))
+        del x, y, card, nz
 
 
 if __name__ == "__main__":

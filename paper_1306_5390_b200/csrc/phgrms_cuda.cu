@@ -124,11 +124,13 @@ FusedFn select_fused(int beta, int T, bool ale) {
     if (beta == B && T == TT) return ale ? fused_ptr<B, TT, true>() : fused_ptr<B, TT, false>();
     PHG_CASE(1, 1) PHG_CASE(1, 2) PHG_CASE(1, 3) PHG_CASE(1, 4) PHG_CASE(1, 5) PHG_CASE(1, 6)
     PHG_CASE(1, 7) PHG_CASE(1, 8) PHG_CASE(2, 1) PHG_CASE(2, 2) PHG_CASE(2, 3) PHG_CASE(2, 4)
+    PHG_CASE(3, 1) PHG_CASE(3, 2)
 #undef PHG_CASE
     return nullptr;
 }
 
-int max_fused(int beta) { return beta == 1 ? 5 : beta == 2 ? 4 : 0; }
+// beta = 3: halo 3T <= kMaxHaloPx and load_row's +-3-byte funnel shifts
+int max_fused(int beta) { return beta == 1 ? 5 : beta == 2 ? 4 : beta == 3 ? 2 : 0; }
 
 // staged rows per tile for the generic kernel (tunable: PHG_ROWS)
 int generic_rows_target() {
@@ -797,11 +799,12 @@ const char* phg_fused_kernel_name(const phg_params* p, int iters) {
                                      "fused_tb_kernel<beta=1,T=5>"};
     static const char* const b2[] = {"", "fused_tb_kernel<beta=2,T=1>", "fused_tb_kernel<beta=2,T=2>",
                                      "fused_tb_kernel<beta=2,T=3>", "fused_tb_kernel<beta=2,T=4>"};
+    static const char* const b3[] = {"", "fused_tb_kernel<beta=3,T=1>", "fused_tb_kernel<beta=3,T=2>"};
     if (!p || iters < 1) return "";
     if (max_fused(p->beta) == 0) return iters == 1 ? "scalar_kernel<fused>" : "";
     if (iters > max_fused(p->beta)) return "";
     if (use_h2(*p, iters)) return h2[iters];
-    return p->beta == 1 ? b1[iters] : b2[iters];
+    return p->beta == 1 ? b1[iters] : p->beta == 2 ? b2[iters] : b3[iters];
 }
 
 int phg_finalize_stats(const uint64_t* ctr, int n, int kcap, phg_pass_stats* stats, int* iterations_run) {
