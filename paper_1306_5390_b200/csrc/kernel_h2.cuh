@@ -73,6 +73,7 @@ struct H2Args {
     uint32_t k7;     // ((256-alpha) & 0x7f) in every byte (candidate pass)
     int m;           // candidate <=> #similar neighbours <= m  (m = min(thr-2, 1))
     int thr;
+    int alpha;       // integer alpha (border pass of fused_h2b2_kernel)
     int it0;
     int kcap;
     unsigned long long* counters;  // [n_images][kcap][2]

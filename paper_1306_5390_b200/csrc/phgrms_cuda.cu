@@ -27,6 +27,7 @@
 #include "kernel_card.cuh"
 #include "kernel_gen.cuh"
 #include "kernel_h2.cuh"
+#include "kernel_h2b2.cuh"
 #include "kernels.cuh"
 
 namespace {
@@ -199,6 +200,19 @@ H2Fn select_h2(int T, bool ale) {
     return nullptr;
 }
 
+template <int T, bool A>
+H2Fn h2b2_ptr() {
+    return phg::fused_h2b2_kernel<T, A>;
+}
+
+H2Fn select_h2b2(int T, bool ale) {
+#define PHG_CASE(TT) \
+    if (T == TT) return ale ? h2b2_ptr<TT, true>() : h2b2_ptr<TT, false>();
+    PHG_CASE(1) PHG_CASE(2) PHG_CASE(3) PHG_CASE(4)
+#undef PHG_CASE
+    return nullptr;
+}
+
 // staged rows per tile for the two-tile fp16 kernel (tunable: PHG_H2_ROWS);
 // 51 rows keep two CTAs (2 x 112.5 KB) resident per SM
 int h2_rows_target() {
@@ -216,6 +230,13 @@ bool use_h2(const phg_params& p, int iters) {
     return !off && p.beta == 1 && p.border == PHG_BORDER_FAITHFUL && p.card_threshold <= 3 && iters <= 5;
 }
 
+// beta = 2 on both pipes (kernel_h2b2.cuh): Faithful, card_threshold <= 3
+// (PHG_NO_H2B2=1 forces fused_tb_kernel<2>).
+bool use_h2b2(const phg_params& p, int iters) {
+    static const bool off = getenv("PHG_NO_H2B2") != nullptr;
+    return !off && p.beta == 2 && p.border == PHG_BORDER_FAITHFUL && p.card_threshold <= 3 && iters <= 4;
+}
+
 uint16_t half_bits(float f) {
     // exact for the small integers and halves used here
     uint32_t u;
@@ -231,10 +252,10 @@ const phg::HaloPeers kNoPeers{};
 
 int launch_h2(const phg_dev_image& src, const phg_dev_image& dst, int row_base, int height, int own_lo,
               int own_hi, const phg_params& p, int it0, int iters, uint64_t* counters, int kcap,
-              cudaStream_t stream, const phg::HaloPeers& peers = kNoPeers) {
-    H2Fn fn = select_h2(iters, p.alpha <= 128);
+              cudaStream_t stream, const phg::HaloPeers& peers = kNoPeers, bool b2 = false) {
+    H2Fn fn = b2 ? select_h2b2(iters, p.alpha <= 128) : select_h2(iters, p.alpha <= 128);
     if (!fn) return fail(PHG_EINVAL, "no two-tile kernel for this iteration count");
-    const int halo = iters;
+    const int halo = b2 ? 2 * iters : iters;
     const Launch L = plan_rows_h2(own_hi - own_lo, halo, h2_rows_target(), src.n_images,
                                   (src.width + phg::kOutPx - 1) / phg::kOutPx);
     const int sh = L.th + 2 * halo;
@@ -264,6 +285,7 @@ int launch_h2(const phg_dev_image& src, const phg_dev_image& dst, int row_base, 
     a.k7 = ((256u - static_cast<uint32_t>(p.alpha)) & 0x7fu) * 0x01010101u;
     a.m = std::min(p.card_threshold - 2, 1);
     a.thr = p.card_threshold;
+    a.alpha = p.alpha;
     a.it0 = it0;
     a.kcap = kcap;
     a.counters = reinterpret_cast<unsigned long long*>(counters);
@@ -382,6 +404,9 @@ int launch_fused(const phg_dev_image& src, const phg_dev_image& dst, int row_bas
     if (use_h2(p, iters))
         return launch_h2(src, dst, row_base, height, own_lo, own_hi, p, it0, iters, counters, kcap, stream,
                          peers);
+    if (use_h2b2(p, iters))
+        return launch_h2(src, dst, row_base, height, own_lo, own_hi, p, it0, iters, counters, kcap, stream,
+                         peers, true);
     FusedFn fn = select_fused(p.beta, iters, p.alpha <= 128);
     if (!fn) return fail(PHG_EINVAL, "no fused kernel for this beta / iteration count");
     const int halo = p.beta * iters;
@@ -803,7 +828,10 @@ const char* phg_fused_kernel_name(const phg_params* p, int iters) {
     if (!p || iters < 1) return "";
     if (max_fused(p->beta) == 0) return iters == 1 ? "scalar_kernel<fused>" : "";
     if (iters > max_fused(p->beta)) return "";
+    static const char* const h2b2[] = {"", "fused_h2b2_kernel<T=1>", "fused_h2b2_kernel<T=2>",
+                                       "fused_h2b2_kernel<T=3>", "fused_h2b2_kernel<T=4>"};
     if (use_h2(*p, iters)) return h2[iters];
+    if (use_h2b2(*p, iters)) return h2b2[iters];
     return p->beta == 1 ? b1[iters] : p->beta == 2 ? b2[iters] : b3[iters];
 }
 
