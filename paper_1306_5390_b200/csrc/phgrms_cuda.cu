@@ -1196,12 +1196,18 @@ int denoise_rows_pipelined(DeviceState* s, const uint8_t* img, int w, int h, con
     for (int i = 0; i < 3; ++i) PHG_CUDA(cudaStreamWaitEvent(s->pipe[i], s->ev0, 0));
     uint8_t* stin = static_cast<uint8_t*>(pin);
     uint8_t* stout = static_cast<uint8_t*>(pout);
+    const bool dense = pitch == w;  // rows already 16-byte pitched: copy straight in and out
     for (int q = 0; q < npieces; ++q) {
         const int64_t rows = rp[q + 1] - rp[q];
-        PHG_CUDA(cudaMemcpyAsync(stin + static_cast<int64_t>(rp[q]) * w, img + static_cast<int64_t>(rp[q]) * w, rows * w,
-                                 cudaMemcpyHostToDevice, sin));
-        PHG_TRY(launch_pitch(stin + static_cast<int64_t>(rp[q]) * w, bufs[0].data + rp[q] * pitch, w, pitch, rows, true,
-                             sin));
+        if (dense) {
+            PHG_CUDA(cudaMemcpyAsync(bufs[0].data + rp[q] * pitch, img + static_cast<int64_t>(rp[q]) * w, rows * w,
+                                     cudaMemcpyHostToDevice, sin));
+        } else {
+            PHG_CUDA(cudaMemcpyAsync(stin + static_cast<int64_t>(rp[q]) * w, img + static_cast<int64_t>(rp[q]) * w,
+                                     rows * w, cudaMemcpyHostToDevice, sin));
+            PHG_TRY(launch_pitch(stin + static_cast<int64_t>(rp[q]) * w, bufs[0].data + rp[q] * pitch, w, pitch, rows,
+                                 true, sin));
+        }
         PHG_CUDA(cudaEventRecord(s->rin[q], sin));
     }
     // launch l reads bufs[in(l)] and writes bufs[outb(l)]: 0 -> 1 -> 2 -> 1 -> 2 ...
@@ -1222,10 +1228,15 @@ int denoise_rows_pipelined(DeviceState* s, const uint8_t* img, int w, int h, con
                 PHG_CUDA(cudaEventRecord(s->rcomp[c], scomp));
                 PHG_CUDA(cudaStreamWaitEvent(sout, s->rcomp[c], 0));
                 const int64_t rows = rc[c + 1] - rc[c];
-                uint8_t* st = stout + static_cast<int64_t>(rc[c]) * w;
-                PHG_TRY(launch_pitch(bufs[outb(l)].data + rc[c] * pitch, st, w, pitch, rows, false, sout));
-                PHG_CUDA(cudaMemcpyAsync(out + static_cast<int64_t>(rc[c]) * w, st, rows * w, cudaMemcpyDeviceToHost,
-                                         sout));
+                if (dense) {
+                    PHG_CUDA(cudaMemcpyAsync(out + static_cast<int64_t>(rc[c]) * w, bufs[outb(l)].data + rc[c] * pitch,
+                                             rows * w, cudaMemcpyDeviceToHost, sout));
+                } else {
+                    uint8_t* st = stout + static_cast<int64_t>(rc[c]) * w;
+                    PHG_TRY(launch_pitch(bufs[outb(l)].data + rc[c] * pitch, st, w, pitch, rows, false, sout));
+                    PHG_CUDA(cudaMemcpyAsync(out + static_cast<int64_t>(rc[c]) * w, st, rows * w,
+                                             cudaMemcpyDeviceToHost, sout));
+                }
             }
         }
     }
@@ -1238,22 +1249,29 @@ int denoise_rows_pipelined(DeviceState* s, const uint8_t* img, int w, int h, con
 }
 
 // Row pieces (copy-in) and chunks (compute + copy-out) for one image; 0
-// chunks = not worth pipelining: below 32 MB the host-side enqueue cost of
-// the extra copies and launches exceeds the overlap (4K image: 97 K plain vs
-// 83-99 K pipelined, measured).  Pieces ~2 MB+ (<= 16), chunks ~8 MB+
-// (<= 8), never shorter than 32 rows.  PHG_ROW_CHUNKS overrides.
+// chunks = not worth pipelining (below 4 MB).  4-32 MB: 3 chunks over 8
+// pieces (C2 4K image e2e: 98 K plain, 118 K pipelined; 2-8 chunks x 4-16
+// pieces measured 109-118 K).  Larger: pieces ~2 MB+ (<= 16), chunks ~8 MB+
+// (<= 8), never shorter than 32 rows.  PHG_ROW_CHUNKS / PHG_ROW_PIECES
+// override.  Rows already 16-byte pitched (width % 16 == 0) are copied
+// straight into / out of the pitched buffers.
 void row_plan_for(int w, int h, int& nchunks, int& npieces) {
-    static const int env = [] {
-        const char* e = getenv("PHG_ROW_CHUNKS");
-        return e ? std::max(0, std::min(8, atoi(e))) : -1;
-    }();
+    const char* ev = getenv("PHG_ROW_CHUNKS");  // read per call (tuning sweeps)
+    const int env = ev ? std::max(0, std::min(8, atoi(ev))) : -1;
+    const char* pv = getenv("PHG_ROW_PIECES");
     const int64_t bytes = static_cast<int64_t>(w) * h;
     nchunks = npieces = 0;
     if (env == 0 || h < 64) return;
-    if (env < 0 && bytes < (int64_t(32) << 20)) return;
+    if (env < 0 && bytes < (int64_t(4) << 20)) return;
+    if (env < 0 && bytes < (int64_t(32) << 20)) {  // 4K-class images: 3 chunks, 8 pieces (C2: 98 -> 118 K)
+        nchunks = std::max(1, std::min(3, h / 32));
+        npieces = std::max(nchunks, std::min(8, h / 32));
+        return;
+    }
     nchunks = env > 0 ? env : static_cast<int>(std::min<int64_t>(8, bytes >> 23));
     nchunks = std::max(1, std::min(nchunks, h / 32));
     npieces = static_cast<int>(std::max<int64_t>(nchunks, std::min<int64_t>(kMaxRowChunks, bytes >> 21)));
+    if (pv) npieces = std::max(1, std::min(kMaxRowChunks, atoi(pv)));
     npieces = std::min(npieces, h / 32);
     npieces = std::max(npieces, nchunks);
 }
