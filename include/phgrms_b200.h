@@ -107,8 +107,9 @@ int phg_denoise_batch(const uint8_t* imgs, int n, int width, int height, const p
  * from one process: devices[0..ndev) are the workers of row_blocks
  * (denoise.hpp:97-107).  n > 1 splits the batch into ndev image shards, one
  * host thread per distinct device, no exchange; n == 1 splits the image into
- * ndev row bands with a halo exchanged between devices after every fused
- * launch (peer copies).  A device may appear more than once.  Same outputs
+ * ndev row bands whose halo rows the fused kernels store straight into the
+ * neighbours' buffers (peer stores, phg_halo_peer; bands thinner than the
+ * halo copy them after each launch).  A device may appear more than once.  Same outputs
  * and stats layout as phg_denoise_batch, bit-identical to phg_denoise.
  * Errors: PHG_EINVAL "devices must list at least one GPU", "device D does
  * not exist". */
@@ -158,6 +159,33 @@ const char* phg_fused_kernel_name(const phg_params* p, int iters);
 int phg_dev_fused_step(const phg_dev_image* src, const phg_dev_image* dst, int row_base,
                        int height, int own_lo, int own_hi, const phg_params* p, int it0,
                        int iters, uint64_t* counters, int kcap, void* stream);
+
+/* A halo mirror (multi-GPU row bands): the owned rows [lo, hi) of a launch
+ * are also stored to ptr + (row - row0) * pitch -- the next buffer of a
+ * neighbouring band (same pitch), a peer or CUDA-IPC-mapped pointer, so
+ * the halo exchange rides inside the launch (NVLink stores) instead of
+ * following it. */
+typedef struct phg_halo_peer {
+    uint8_t* ptr;
+    int32_t row0; /* global row of ptr's buffer row 0 */
+    int32_t lo, hi;
+    int32_t _pad;
+} phg_halo_peer;
+
+/* phg_dev_fused_step plus up to two halo mirrors (single-image bands).
+ * The caller orders launches across bands: launch c of a band starts after
+ * launch c-1 of both neighbours has finished. */
+int phg_dev_fused_step_mirrored(const phg_dev_image* src, const phg_dev_image* dst, int row_base,
+                                int height, int own_lo, int own_hi, const phg_params* p, int it0,
+                                int iters, uint64_t* counters, int kcap, const phg_halo_peer* peers,
+                                int npeers, void* stream);
+
+/* CUDA IPC for one-process-per-GPU bands: export a device pointer as a
+ * 64-byte handle + its offset inside the allocation; open it in another
+ * process of the node (returns the mapped pointer incl. the offset); close. */
+int phg_ipc_get_handle(const void* dev_ptr, uint8_t* handle, uint64_t* offset);
+int phg_ipc_open_handle(const uint8_t* handle, uint64_t offset, void** dev_ptr);
+int phg_ipc_close(void* dev_ptr, uint64_t offset);
 
 /* Full k-iteration denoise of whole images resident on the device:
  * reads src, leaves the result in dst, uses tmp as the ping-pong partner

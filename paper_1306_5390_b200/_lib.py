@@ -24,7 +24,8 @@ EXPORTS = (
     "phg_inject_sp_noise", "phg_max_fused_iterations", "phg_dev_fused_step",
     "phg_dev_denoise", "phg_dev_cardinality", "phg_dev_removal", "phg_finalize_stats",
     "phg_fused_kernel_name", "phg_residual_noise_count", "phg_sse", "phg_dev_residual_count", "phg_dev_sse",
-    "phg_dev_synth_smooth", "phg_dev_inject_noise", "phg_denoise_sharded",
+    "phg_dev_synth_smooth", "phg_dev_inject_noise", "phg_denoise_sharded", "phg_dev_fused_step_mirrored",
+    "phg_ipc_get_handle", "phg_ipc_open_handle", "phg_ipc_close",
 )
 
 
@@ -43,6 +44,12 @@ class PhgPassStats(C.Structure):
 class PhgDevImage(C.Structure):
     _fields_ = [("data", C.c_void_p), ("pitch", C.c_int64), ("image_stride", C.c_int64),
                 ("width", C.c_int32), ("rows", C.c_int32), ("n_images", C.c_int32),
+                ("_pad", C.c_int32)]
+
+
+class PhgHaloPeer(C.Structure):
+    """phg_halo_peer: owned rows [lo, hi) mirrored to ptr + (row - row0) * pitch."""
+    _fields_ = [("ptr", C.c_void_p), ("row0", C.c_int32), ("lo", C.c_int32), ("hi", C.c_int32),
                 ("_pad", C.c_int32)]
 
 
@@ -83,6 +90,13 @@ def lib():
         L.phg_denoise_sharded.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(PhgParams),
                                           C.POINTER(C.c_int), C.c_int, C.c_void_p, C.POINTER(PhgPassStats),
                                           C.POINTER(C.c_int)]
+        L.phg_dev_fused_step_mirrored.argtypes = [C.POINTER(PhgDevImage), C.POINTER(PhgDevImage), C.c_int, C.c_int,
+                                                  C.c_int, C.c_int, C.POINTER(PhgParams), C.c_int, C.c_int,
+                                                  C.c_void_p, C.c_int, C.POINTER(PhgHaloPeer), C.c_int,
+                                                  C.c_void_p]
+        L.phg_ipc_get_handle.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64)]
+        L.phg_ipc_open_handle.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_void_p)]
+        L.phg_ipc_close.argtypes = [C.c_void_p, C.c_uint64]
         L.phg_synth_image.argtypes = [C.c_int, C.c_int, C.c_uint32, C.c_int, _u8p]
         L.phg_inject_sp_noise.argtypes = [_u8p, C.c_int, C.c_int, C.c_double, C.c_double, C.c_uint32,
                                           _u8p, C.c_void_p]

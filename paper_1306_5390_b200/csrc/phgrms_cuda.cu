@@ -867,6 +867,72 @@ int phg_dev_fused_step(const phg_dev_image* src, const phg_dev_image* dst, int r
                 static_cast<cudaStream_t>(stream));
 }
 
+int phg_dev_fused_step_mirrored(const phg_dev_image* src, const phg_dev_image* dst, int row_base, int height,
+                                int own_lo, int own_hi, const phg_params* p, int it0, int iters,
+                                uint64_t* counters, int kcap, const phg_halo_peer* peers, int npeers,
+                                void* stream) {
+    PHG_TRY(validate(p));
+    if (!src || !dst || own_lo < 0 || own_hi > height || own_lo >= own_hi || iters < 1 || it0 < 0 ||
+        it0 + iters > kcap)
+        return fail(PHG_EINVAL, "bad band geometry");
+    if (max_fused(p->beta) > 0 && iters > max_fused(p->beta))
+        return fail(PHG_EINVAL, "iters exceeds phg_max_fused_iterations(beta)");
+    if (npeers < 0 || npeers > 2 || (npeers > 0 && !peers)) return fail(PHG_EINVAL, "at most two halo peers");
+    if (dst->n_images != 1) return fail(PHG_EINVAL, "halo peers need single-image bands");
+    phg::HaloPeers hp{};
+    for (int i = 0; i < npeers; ++i) {
+        if (!peers[i].ptr || peers[i].lo < own_lo || peers[i].hi > own_hi)
+            return fail(PHG_EINVAL, "halo peer rows must be owned rows");
+        hp.ptr[i] = peers[i].ptr;
+        hp.row0[i] = peers[i].row0;
+        hp.lo[i] = peers[i].lo;
+        hp.hi[i] = peers[i].hi;
+    }
+    return step(*src, *dst, row_base, height, own_lo, own_hi, *p, it0, iters, counters, kcap,
+                static_cast<cudaStream_t>(stream), hp);
+}
+
+// CUDA IPC: a band buffer allocated by one process mapped into another (one
+// process per GPU on an NVSwitch node).  Handles name whole allocations, so
+// the pointer's offset inside its allocation travels with the handle.
+int phg_ipc_get_handle(const void* dev_ptr, uint8_t* handle, uint64_t* offset) {
+    if (!dev_ptr || !handle || !offset) return fail(PHG_EINVAL, "null argument");
+    static PFN_cuMemGetAddressRange_v3020 range = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        return cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+                       q == cudaDriverEntryPointSuccess
+                   ? reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(fn)
+                   : nullptr;
+    }();
+    if (!range) return fail(PHG_ENODEV, "cuMemGetAddressRange unavailable");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+        return fail(PHG_EINVAL, "not a device allocation");
+    cudaIpcMemHandle_t h;
+    PHG_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+    std::memcpy(handle, &h, sizeof(h));
+    *offset = reinterpret_cast<uint64_t>(dev_ptr) - static_cast<uint64_t>(base);
+    return PHG_OK;
+}
+
+int phg_ipc_open_handle(const uint8_t* handle, uint64_t offset, void** dev_ptr) {
+    if (!handle || !dev_ptr) return fail(PHG_EINVAL, "null argument");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    void* base = nullptr;
+    PHG_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    *dev_ptr = static_cast<uint8_t*>(base) + offset;
+    return PHG_OK;
+}
+
+int phg_ipc_close(void* dev_ptr, uint64_t offset) {
+    if (!dev_ptr) return fail(PHG_EINVAL, "null argument");
+    PHG_CUDA(cudaIpcCloseMemHandle(static_cast<uint8_t*>(dev_ptr) - offset));
+    return PHG_OK;
+}
+
 int phg_dev_denoise(const phg_dev_image* src, const phg_dev_image* dst, const phg_dev_image* tmp,
                     const phg_params* p, uint64_t* counters, void* stream) {
     PHG_TRY(validate(p));

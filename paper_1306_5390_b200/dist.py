@@ -141,19 +141,107 @@ def truncate_stats(counters) -> List[Tuple[int, int]]:
 
 
 # ------------------------------------------------------------ GPU stepper
-def cuda_band_stepper(params, counters: torch.Tensor, width: int, height: int, stream=None) -> Stepper:
+def cuda_band_stepper(params, counters: torch.Tensor, width: int, height: int, stream=None):
     """Stepper running the fused sm_100a kernel (phg_dev_fused_step) on band
-    buffers that live on the current CUDA device.  counters: int64 [k, 2]."""
-    from ._lib import PhgDevImage, check, lib
+    buffers that live on the current CUDA device.  counters: int64 [k, 2].
+    With ``peers`` (a list of PhgHaloPeer) the launch also stores the owned
+    rows that lie in the neighbours' halos into their buffers
+    (phg_dev_fused_step_mirrored)."""
+    from ._lib import PhgDevImage, PhgHaloPeer, check, lib
 
     L = lib()
     kcap = counters.shape[0]
 
-    def step(src, dst, plan, it0, iters):
+    def step(src, dst, plan, it0, iters, peers=None):
         s = PhgDevImage(src.data_ptr(), src.stride(0), src.stride(0) * plan.rows, width, plan.rows, 1, 0)
         d = PhgDevImage(dst.data_ptr(), dst.stride(0), dst.stride(0) * plan.rows, width, plan.rows, 1, 0)
         st = stream if stream is not None else torch.cuda.current_stream().cuda_stream
-        check(L.phg_dev_fused_step(C.byref(s), C.byref(d), plan.blo, height, plan.lo, plan.hi, C.byref(params),
-                                   it0, iters, C.c_void_p(counters.data_ptr()), kcap, C.c_void_p(st)))
+        if peers:
+            arr = (PhgHaloPeer * len(peers))(*peers)
+            check(L.phg_dev_fused_step_mirrored(C.byref(s), C.byref(d), plan.blo, height, plan.lo, plan.hi,
+                                                C.byref(params), it0, iters, C.c_void_p(counters.data_ptr()),
+                                                kcap, arr, len(peers), C.c_void_p(st)))
+        else:
+            check(L.phg_dev_fused_step(C.byref(s), C.byref(d), plan.blo, height, plan.lo, plan.hi,
+                                       C.byref(params), it0, iters, C.c_void_p(counters.data_ptr()), kcap,
+                                       C.c_void_p(st)))
 
     return step
+
+
+# ------------------------------------------- fused halo exchange (CUDA IPC)
+def mirror_rows(plan: BandPlan, other: BandPlan) -> Tuple[int, int]:
+    """Global rows of `plan`'s band that lie in the halo of the neighbouring
+    band `other` ([lo, hi), possibly empty)."""
+    return max(plan.lo, other.blo), min(plan.hi, other.bhi)
+
+
+class IpcHaloPeers:
+    """The neighbours' ping-pong band buffers mapped into this process with
+    CUDA IPC (one process per GPU on an NVSwitch node), as PhgHaloPeer lists
+    for the mirrored stepper: launch i of every rank writes the rows its
+    neighbours need straight into their buffer i % 2 -- NVLink stores issued
+    by the kernel epilogue -- so no exchange step follows the launch.
+
+    ``bufs`` are this rank's two [rows, pitch] uint8 CUDA tensors; all ranks
+    of ``group`` call the constructor (it all-gathers the handles)."""
+
+    def __init__(self, plan: BandPlan, bufs, group=None):
+        from ._lib import PhgHaloPeer, check, lib
+
+        L = lib()
+        self.L, self.plan = L, plan
+        mine = []
+        for b in bufs:
+            h = (C.c_uint8 * 64)()
+            off = C.c_uint64()
+            check(L.phg_ipc_get_handle(C.c_void_p(b.data_ptr()), h, C.byref(off)))
+            mine.append((bytes(h), int(off.value), int(b.stride(0))))
+        world = dist.get_world_size(group)
+        allh = [None] * world
+        dist.all_gather_object(allh, (plan.rank, plan.blo, plan.bhi, mine), group=group)
+        self.opened = []
+        self.peers = [[], []]  # per parity
+        for nb in (plan.up, plan.down):
+            if nb is None:
+                continue
+            rank, blo, bhi, hs = allh[nb]
+            other = BandPlan(plan.height, plan.width, plan.world, rank, plan.halo)
+            lo, hi = mirror_rows(plan, other)
+            for parity, (hb, off, pitch) in enumerate(hs):
+                if pitch != bufs[parity].stride(0):
+                    raise ValueError("band buffers must share one pitch")
+                ptr = C.c_void_p()
+                check(L.phg_ipc_open_handle((C.c_uint8 * 64).from_buffer_copy(hb), off, C.byref(ptr)))
+                self.opened.append((ptr.value, off))
+                if hi > lo:
+                    self.peers[parity].append(PhgHaloPeer(ptr.value, blo, lo, hi, 0))
+
+    def for_buffer(self, parity: int):
+        return self.peers[parity]
+
+    def close(self):
+        for ptr, off in self.opened:
+            self.L.phg_ipc_close(C.c_void_p(ptr), off)
+        self.opened = []
+
+
+def denoise_band_fused(src: torch.Tensor, bufs, plan: BandPlan, k: int, tmax: int, stepper, peers: IpcHaloPeers,
+                       group=None) -> torch.Tensor:
+    """denoise_band with the halo exchange fused into the launches: launch i
+    writes bufs[i % 2] and, through the IPC mirrors, the neighbours'
+    bufs[i % 2] halo rows.  Between launches one host barrier orders launch i
+    of every rank after launch i-1 of its neighbours (they read the rows the
+    next launch overwrites, and write the rows it reads)."""
+    cur = src
+    it0 = 0
+    launches = chunk_plan(k, tmax)
+    for i, iters in enumerate(launches):
+        if i > 0:
+            torch.cuda.current_stream().synchronize()
+            dist.barrier(group=group)
+        last = i + 1 == len(launches)  # the last launch's halos are never read
+        stepper(cur, bufs[i % 2], plan, it0, iters, None if last else peers.for_buffer(i % 2))
+        cur = bufs[i % 2]
+        it0 += iters
+    return cur
