@@ -27,8 +27,8 @@
 // therefore ignores the image edges entirely -- cells outside the image hold
 // whatever was staged (TMA zero fill) and only corrupt the counts of border
 // pixels -- and candidates are masked to interior pixels.  The flagged
-// border pixels a tile owns are counted exactly by a separate scalar pass
-// (b2_border_pass), a few hundred pixels per edge tile.
+// border pixels a tile owns are counted exactly by a scalar pass at the end
+// of every iteration (the <= 4 border rows / columns of edge tiles).
 //
 // Candidates (interior, <= m similar neighbours, m = min(thr - 2, 1)) are
 // flagged and replaced: flag >= 23 > 22.  They are compacted into the
