@@ -232,6 +232,13 @@ int phg_dev_synth_smooth(const phg_dev_image* out, int row_base, int height, uin
 int phg_dev_inject_noise(const phg_dev_image* img, int row_base, int height, double density,
                          double salt_ratio, uint64_t seed, uint64_t* count, void* stream);
 
+/* Diagnostic: out[S] = the fused kernels' device RMS replacement
+ * round(sqrt(S/f)) (kernel_h2.cuh h2_rms, used by the beta = 1 and beta = 2
+ * fused kernels) for every S in [0, n); f in {7, 8, 23, 24}, n <= 2^21.
+ * The parity tests compare it with the reference's llround(sqrt(double(S)/f))
+ * (denoise.hpp:163-169) exhaustively. */
+int phg_debug_rms(int f, uint32_t n, uint32_t* out);
+
 /* Turn device counters into reference PassStats: per image, truncate after
  * the first iteration with replaced == 0 (denoise.hpp:308). */
 int phg_finalize_stats(const uint64_t* host_counters, int n_images, int kcap,

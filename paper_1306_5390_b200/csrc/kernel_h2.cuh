@@ -158,18 +158,21 @@ __device__ __forceinline__ void h2_pairs_down(const uint32_t (&v)[6], const uint
 }
 
 // round(sqrt(S/f)) half away from zero (denoise.hpp:163-169), branch-free,
-// for 4S < 2^23 and f in {7, 8}: r ~ sqrt(4S/f) (MUFU.SQRT, rel. error
-// ~2^-22), m = nearest(r); the answer floor((sqrt(4S/f)+1)/2) is u0 =
-// (m+1)>>1 unless m is odd and sqrt(4S/f) < m, i.e. (2u0-1)^2 f > 4S -- an
-// exact integer test that is never true for even m.
+// for S < 2^23 and f in {7, 8} (beta = 1) or {23, 24} (beta = 2), rcp_f =
+// fp32(1/f).  r ~ sqrt(S/f): one rounding in rcp_f, one in the product and
+// MUFU.SQRT's own error, together a relative error below 2^-21.  Scaling r by
+// 1 + 2^-20 inside the rounding FFMA lifts it strictly above the exact root
+// and by less than 273 * 2^-19 < 1/2, so n = nearest(r (1 + 2^-20)) is the
+// exact u = floor(sqrt(S/f) + 1/2) or u + 1, and u = n - [n > 0 and
+// (2n-1)^2 f > 4S] (an exact integer test).  Exhaustively checked on the GPU
+// for every S up to 24 * 65025 (tests/test_parity_gpu.py, phg_debug_rms).
 __device__ __forceinline__ uint32_t h2_rms(uint32_t S, uint32_t f, float rcp_f) {
-    const float s4 = __int_as_float(0x4b000000 | (4u * S)) - 8388608.0f;  // exact
+    const float s = __int_as_float(0x4b000000 | S) - 8388608.0f;  // exact
     float r;
-    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(s4 * rcp_f));
-    const int m = max(__float_as_int(r + 12582912.0f) - 0x4b400000, 1);  // nearest (S = 0 -> 1 -> 0)
-    const uint32_t u0 = static_cast<uint32_t>(m + 1) >> 1;
-    const uint32_t q = 2u * u0 - 1u;
-    return u0 - ((q * q * f > 4u * S) ? 1u : 0u);
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(s * rcp_f));
+    const int n = __float_as_int(fmaf(r, 1.00000095367431640625f, 12582912.0f)) - 0x4b400000;
+    const uint32_t q = 2u * static_cast<uint32_t>(n) - 1u;
+    return static_cast<uint32_t>(n) - ((n > 0 && q * q * f > 4u * S) ? 1u : 0u);
 }
 
 __device__ __forceinline__ void sts16(uint32_t addr, uint32_t v) {
@@ -183,11 +186,11 @@ __device__ __forceinline__ uint32_t lds16(uint32_t addr) {
 
 // One candidate pixel (interior, Faithful, beta=1): RMS of the dissimilar
 // cells of its 3x3 window, exactly as removal_rows (denoise.hpp:199-217).
-// `o` = byte offset of the pixel in the interleaved tile; returns the new
-// value (no store, so that two candidates' loads can be interleaved).
+// `o1` = byte offset of the window's top-left cell (the pixel's offset minus
+// kH2RP + 2) in the interleaved tile; returns the new value (no store, so
+// that several candidates' loads can be interleaved).
 template <bool ALE>
-__device__ __forceinline__ uint32_t h2_replace(uint32_t src, int o, uint32_t k7) {
-    const int o1 = o - kH2RP - 2;
+__device__ __forceinline__ uint32_t h2_replace(uint32_t src, int o1, uint32_t k7) {
     const int b4 = o1 & ~3;
     const uint32_t sh = static_cast<uint32_t>(o1 & 3);
     const uint32_t sel = 0x0420u + sh * 0x0111u;  // bytes sh, sh+2, sh+4
@@ -343,7 +346,7 @@ __global__ void __launch_bounds__(kH2Threads, 2)
         int pending = 0;  // warp-uniform: items waiting at ring[0, pending)
         // process ring[h, h+n), n <= kH2Round: three independent candidates per
         // lane, all loads issued before any store.  Items are the byte offsets
-        // of the candidates in the interleaved tile.
+        // of the candidates' window corners in the interleaved tile.
         auto drain = [&](int h, int n) {
             const int o0 = static_cast<int>(lds16(ring + 2 * (h + (lane < n ? lane : 0))));
             const int o1 = static_cast<int>(lds16(ring + 2 * (h + (lane + 32 < n ? lane + 32 : 0))));
@@ -351,9 +354,10 @@ __global__ void __launch_bounds__(kH2Threads, 2)
             const uint32_t v0 = h2_replace<ALE>(src, o0, a.k7);
             const uint32_t v1 = h2_replace<ALE>(src, o1, a.k7);
             const uint32_t v2 = h2_replace<ALE>(src, o2, a.k7);
-            if (lane < n) sts8a(dst + o0, v0);
-            if (lane + 32 < n) sts8a(dst + o1, v1);
-            if (lane + 64 < n) sts8a(dst + o2, v2);
+            const uint32_t dc = dst + kH2RP + 2;  // items are window corners
+            if (lane < n) sts8a(dc + o0, v0);
+            if (lane + 32 < n) sts8a(dc + o1, v1);
+            if (lane + 64 < n) sts8a(dc + o2, v2);
         };
         if (ylo < yhi) {
             const uint32_t colp = src + 16 + 8 * c;
@@ -392,7 +396,8 @@ __global__ void __launch_bounds__(kH2Threads, 2)
                 if (total) {
                     uint32_t addr = ring + 2 * (pending + incl - n);
                     // bit b = 8k + 4h + s: row y0 + 3 - s, column byte k + 4h
-                    const uint32_t base3 = static_cast<uint32_t>((y0 + 3) * kH2RP + 16 + 8 * c);
+                    // items are window corners: pixel offset - kH2RP - 2
+                    const uint32_t base3 = static_cast<uint32_t>((y0 + 2) * kH2RP + 14 + 8 * c);
                     uint32_t mm = R;
                     while (mm) {
                         uint32_t b;

@@ -30,6 +30,12 @@
 #include "kernel_h2b2.cuh"
 #include "kernels.cuh"
 
+// phg_debug_rms: the fused kernels' RMS replacement for every S < n.
+__global__ void rms_probe_kernel(uint32_t f, float rcp_f, uint32_t n, uint32_t* out) {
+    const uint32_t S = blockIdx.x * blockDim.x + threadIdx.x;
+    if (S < n) out[S] = phg::h2_rms(S, f, rcp_f);
+}
+
 namespace {
 
 thread_local std::string g_error;
@@ -1158,6 +1164,24 @@ int phg_residual_noise_count(const uint8_t* img, int w, int h, int alpha, int be
     PHG_CUDA(cudaMemsetAsync(pk, 0, sizeof(uint64_t), s->stream));
     PHG_TRY(phg_dev_residual_count(&im, alpha, beta, card_threshold, static_cast<uint64_t*>(pk), s->stream));
     PHG_CUDA(cudaMemcpyAsync(count, pk, sizeof(uint64_t), cudaMemcpyDeviceToHost, s->stream));
+    PHG_CUDA(cudaStreamSynchronize(s->stream));
+    return PHG_OK;
+}
+
+int phg_debug_rms(int f, uint32_t n, uint32_t* out) {
+    if (!out) return fail(PHG_EINVAL, "null argument");
+    if ((f != 7 && f != 8 && f != 23 && f != 24) || n > (1u << 21))
+        return fail(PHG_EINVAL, "phg_debug_rms: f in {7, 8, 23, 24}, n <= 2^21");
+    if (n == 0) return PHG_OK;
+    DeviceState* s;
+    PHG_TRY(current_state(&s));
+    void* pd;
+    PHG_TRY(scratch(s, 4, sizeof(uint32_t) * n, &pd));
+    rms_probe_kernel<<<(n + 255) / 256, 256, 0, s->stream>>>(static_cast<uint32_t>(f), 1.0f / static_cast<float>(f),
+                                                              n, static_cast<uint32_t*>(pd));
+    ++g_launches;
+    PHG_CUDA(cudaGetLastError());
+    PHG_CUDA(cudaMemcpyAsync(out, pd, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, s->stream));
     PHG_CUDA(cudaStreamSynchronize(s->stream));
     return PHG_OK;
 }

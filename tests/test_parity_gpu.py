@@ -240,3 +240,32 @@ def test_generators_match_oracle():
         assert np.array_equal(a.pixels, O.synth_image(97, 61, seed))
         n1 = P.inject_sp_noise(a, P.NoiseSpec(0.3, 0.5, seed))
         assert np.array_equal(n1.pixels, O.inject_sp_noise(a.pixels, 0.3, 0.5, seed))
+
+
+# ------------------------------------------- device RMS, exhaustive (h2_rms)
+def _rms_exact(S, f):
+    """u = llround(sqrt(S/f)) (denoise.hpp:163-169) as the integer rule
+    max u: (2u-1)^2 f <= 4S (pinned against the reference's double formula
+    in tests/test_abi.py)."""
+    S = S.astype(np.int64)
+    u = np.floor((np.sqrt(4.0 * S / f) + 1.0) / 2.0).astype(np.int64)
+    u -= ((u >= 1) & ((2 * u - 1) ** 2 * f > 4 * S)).astype(np.int64)
+    u += ((2 * u + 1) ** 2 * f <= 4 * S).astype(np.int64)
+    return u
+
+
+@pytest.mark.parametrize("f", [7, 8, 23, 24])
+def test_device_rms_exhaustive(f):
+    """Every S the fused kernels can meet (S <= f * 65025: f dissimilar cells
+    of at most 255) gives the reference's rounding bit for bit."""
+    import ctypes as C
+    from paper_1306_5390_b200._lib import lib
+    n = f * 65025 + 1
+    out = np.empty(n, np.uint32)
+    assert lib().phg_debug_rms(f, n, out.ctypes.data_as(C.c_void_p)) == 0
+    S = np.arange(n, dtype=np.int64)
+    ref = _rms_exact(S, f)
+    bad = np.nonzero(out.astype(np.int64) != ref)[0]
+    assert bad.size == 0, [(int(s), int(out[s]), int(ref[s])) for s in bad[:8]]
+    for s in (0, 1, 2, 3, 4 * f - 1, 4 * f, f * 65025, 12345):
+        assert int(out[s]) == O.rms_replacement(s, f), s
