@@ -14,8 +14,8 @@ A step = one full k=5 denoise of this rank's batch (default workload c4:
   e2e       the same metric through the public host-buffer C ABI
             (phg_denoise_batch from pinned host memory: H2D, kernels, D2H of
             the images and per-iteration counters inside the timed region).
-  roofline  the dominant kernel (fused_h2_kernel for beta=1 / fused_tb_kernel for beta=2,
-            T iterations per launch)
+  roofline  the dominant kernel (fused_h2_kernel for beta=1 / fused_h2b2_kernel for
+            beta=2, T iterations per launch)
             against MEASURED_PEAKS.json hbm_gbs, algorithmic bytes = 2 B per
             pixel-iteration.
   cpu_baseline  the reference's own CPU path (oracle/_ref, compiled from the
