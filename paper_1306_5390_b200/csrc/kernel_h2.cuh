@@ -15,7 +15,10 @@
 // once and credited to both ends (E, S, SE, SW pairs; 4 tests per pixel
 // instead of 8).  The ALU pipe only converts bytes to halves (one PRMT per
 // pair of pixels) and extracts candidate bits, so it is free for the RMS
-// replacement of the ~13% candidate pixels (byte-SIMD, as before).
+// replacement of the ~13% candidate pixels (byte-SIMD, as before).  In rows
+// whose window is inside the image the vertical (S) pairs, which are whole
+// interleaved words apart, run in byte-SIMD on the ALU pipe instead, to
+// balance the two pipes.
 //
 // Two tiles per CTA: lane 0 of every half2 holds tile A, lane 1 tile B (the
 // next tile in the (image, row tile, column tile) order), so each lane is an
@@ -298,6 +301,9 @@ __global__ void __launch_bounds__(kH2Threads, 2)
         colint |= (nA ? 1u : 0u) << bA | (nB ? 1u : 0u) << bB;
     }
     const uint32_t neg64 = 0xd400d400u;  // half2(-64, -64)
+    uint32_t ckF[4];  // fast rows: counts carry -18 (two -9 credits)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) ckF[j] = h2add(ck[j], 0xcc80cc80u);  // half2(-18)
 
     __syncthreads();  // barrier init + counters visible
     mbar_wait(&bar, 0);
@@ -433,13 +439,38 @@ __global__ void __launch_bounds__(kH2Threads, 2)
                 uint32_t e[5];
 #pragma unroll
                 for (int i = 0; i < 5; ++i) e[i] = h2sim(v[i], v[i + 1], a.alpha2);
-                uint32_t s[4], d[5], aa[5];
-                h2_pairs_down(v, nv, a.alpha2, s, d, aa);
                 uint32_t cnt[4];
+                if constexpr (FAST) {
+                    // S pairs (y, j)-(y+1, j) on the ALU pipe: byte-SIMD test of
+                    // the raw interleaved words, dissimilar bytes 0x80 become the
+                    // halves 1024 + 128 dis (one PRMT), credited by
+                    // fma(., -1/128, .) = -8 - dis = s - 9.  Counts in this loop
+                    // carry -9 per credit (up[] too), compared against ckF = ck - 18.
+                    const uint32_t d0 = __vabsdiffu4(raw.x, nraw.x), d1 = __vabsdiffu4(raw.y, nraw.y);
+                    const uint32_t t0 = (d0 & kLo7) + a.k7, t1 = (d1 & kLo7) + a.k7;
+                    const uint32_t x0 = (ALE ? (d0 | t0) : (d0 & t0)) & kHi;
+                    const uint32_t x1 = (ALE ? (d1 | t1) : (d1 & t1)) & kHi;
+                    const uint32_t sv[4] = {prmt(x0, 0x64646464u, 0x4140), prmt(x0, 0x64646464u, 0x4342),
+                                            prmt(x1, 0x64646464u, 0x4140), prmt(x1, 0x64646464u, 0x4342)};
+                    uint32_t d[5], aa[5];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    cnt[j] = h2add(h2add(h2add(e[j], e[j + 1]), h2add(s[j], d[j + 1])), h2add(aa[j], up[j]));
-                    up[j] = h2add(h2add(s[j], d[j]), aa[j + 1]);
+                    for (int i = 0; i < 5; ++i) d[i] = h2sim(v[i], nv[i + 1], a.alpha2);
+#pragma unroll
+                    for (int i = 0; i < 5; ++i) aa[i] = h2sim(v[i + 1], nv[i], a.alpha2);
+                    constexpr uint32_t m128 = 0xa000a000u;  // half2(-1/128)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        cnt[j] = h2add(h2add(h2add(e[j], e[j + 1]), h2fma(sv[j], m128, d[j + 1])), h2add(aa[j], up[j]));
+                        up[j] = h2fma(sv[j], m128, h2add(d[j], aa[j + 1]));
+                    }
+                } else {  // rows with out-of-image cells: every pair in fp16
+                    uint32_t s[4], d[5], aa[5];
+                    h2_pairs_down(v, nv, a.alpha2, s, d, aa);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        cnt[j] = h2add(h2add(h2add(e[j], e[j + 1]), h2add(s[j], d[j + 1])), h2add(aa[j], up[j]));
+                        up[j] = h2add(h2add(s[j], d[j]), aa[j + 1]);
+                    }
                 }
                 // the centre row goes to the destination unchanged (candidates are
                 // overwritten by the replacement pass)
@@ -459,7 +490,7 @@ __global__ void __launch_bounds__(kH2Threads, 2)
                 uint32_t vn[4];
                 if (FAST) {
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(vn[j]) : "r"(cnt[j]), "r"(ck[j]));
+                    for (int j = 0; j < 4; ++j) asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(vn[j]) : "r"(cnt[j]), "r"(ckF[j]));
                 } else {
                     const int ra = gyA + y, rb = gyB + y;
                     const bool iA = ra >= 1 && ra < H - 1, iB = hasB && rb >= 1 && rb < H - 1;
@@ -489,8 +520,13 @@ __global__ void __launch_bounds__(kH2Threads, 2)
             const int s0 = min(max(ylo, f_lo), yhi);
             const int s1 = max(min(yhi, f_hi), s0);
             for (int y = ylo; y < s0; ++y) row(y, std::false_type{});
+            constexpr uint32_t m9 = 0xc880c880u;  // half2(-9): the fast rows' credit offset
+#pragma unroll
+            for (int j = 0; j < 4; ++j) up[j] = h2add(up[j], m9);
 #pragma unroll 2
             for (int y = s0; y < s1; ++y) row(y, std::true_type{});
+#pragma unroll
+            for (int j = 0; j < 4; ++j) up[j] = h2add(up[j], 0x48804880u);  // half2(+9)
             for (int y = s1; y < yhi; ++y) row(y, std::false_type{});
             if (yhi & 3) {  // a partial last quad: rows (yhi & ~3) .. yhi-1
                 R <<= 4 - (yhi & 3);
