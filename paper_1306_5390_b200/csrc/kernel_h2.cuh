@@ -405,12 +405,19 @@ __global__ void __launch_bounds__(kH2Threads, 2)
                     // items are window corners: pixel offset - kH2RP - 2
                     const uint32_t base3 = static_cast<uint32_t>((y0 + 2) * kH2RP + 14 + 8 * c);
                     uint32_t mm = R;
+                    // two items per trip: the second store is predicated on a
+                    // remaining bit (bfind of 0 is ~0u; shl.b32 by >= 32 gives 0)
                     while (mm) {
-                        uint32_t b;
+                        uint32_t b, b2, m1, m2;
                         asm("bfind.u32 %0, %1;" : "=r"(b) : "r"(mm));
-                        mm ^= 1u << b;
+                        asm("shl.b32 %0, 1, %1;" : "=r"(m1) : "r"(b));
+                        mm ^= m1;
+                        asm("bfind.u32 %0, %1;" : "=r"(b2) : "r"(mm));
+                        asm("shl.b32 %0, 1, %1;" : "=r"(m2) : "r"(b2));
                         sts16(addr, base3 - (b & 3u) * kH2RP + (b >> 3) + (b & 4u));
-                        addr += 2;
+                        if (mm) sts16(addr + 2, base3 - (b2 & 3u) * kH2RP + (b2 >> 3) + (b2 & 4u));
+                        mm ^= m2;
+                        addr += 4;
                     }
                     pending += total;
                     __syncwarp();
