@@ -53,6 +53,10 @@ constexpr int kH2MaxRows = 62;            // ring items are u16 byte offsets: sh
 // the two [sh][528] tiles (B at a 128-byte aligned offset)
 __host__ __device__ constexpr int h2_stage_b(int sh) { return (kRP * sh + 127) / 128 * 128; }
 __host__ __device__ constexpr int h2_buf_bytes(int sh) { return (kH2RP * sh + 128 + 127) / 128 * 128; }
+#ifndef PHG_PUSH_UNROLL
+#define PHG_PUSH_UNROLL 3
+#endif
+constexpr int kH2PushUnroll = PHG_PUSH_UNROLL;  // candidates per push-loop trip
 constexpr int kH2Round = 96;           // drained per round: three candidates per lane
 constexpr int kH2Ring = kH2Round + 32 * 32;  // per-warp u16 items: leftovers + one row quad
 __host__ __device__ constexpr int h2_smem_bytes(int sh) {
@@ -405,19 +409,19 @@ __global__ void __launch_bounds__(kH2Threads, 2)
                     // items are window corners: pixel offset - kH2RP - 2
                     const uint32_t base3 = static_cast<uint32_t>((y0 + 2) * kH2RP + 14 + 8 * c);
                     uint32_t mm = R;
-                    // two items per trip: the second store is predicated on a
-                    // remaining bit (bfind of 0 is ~0u; shl.b32 by >= 32 gives 0)
+                    // kH2PushUnroll items per loop trip: the first store always
+                    // has a bit, the others are predicated on a remaining bit
+                    // (bfind of 0 is ~0u; shl.b32 by >= 32 gives 0)
                     while (mm) {
-                        uint32_t b, b2, m1, m2;
-                        asm("bfind.u32 %0, %1;" : "=r"(b) : "r"(mm));
-                        asm("shl.b32 %0, 1, %1;" : "=r"(m1) : "r"(b));
-                        mm ^= m1;
-                        asm("bfind.u32 %0, %1;" : "=r"(b2) : "r"(mm));
-                        asm("shl.b32 %0, 1, %1;" : "=r"(m2) : "r"(b2));
-                        sts16(addr, base3 - (b & 3u) * kH2RP + (b >> 3) + (b & 4u));
-                        if (mm) sts16(addr + 2, base3 - (b2 & 3u) * kH2RP + (b2 >> 3) + (b2 & 4u));
-                        mm ^= m2;
-                        addr += 4;
+#pragma unroll
+                        for (int u = 0; u < kH2PushUnroll; ++u) {
+                            uint32_t b, m1;
+                            asm("bfind.u32 %0, %1;" : "=r"(b) : "r"(mm));
+                            asm("shl.b32 %0, 1, %1;" : "=r"(m1) : "r"(b));
+                            if (u == 0 || mm) sts16(addr + 2 * u, base3 - (b & 3u) * kH2RP + (b >> 3) + (b & 4u));
+                            mm ^= m1;
+                        }
+                        addr += 2 * kH2PushUnroll;
                     }
                     pending += total;
                     __syncwarp();

@@ -43,6 +43,11 @@
 
 namespace phg {
 
+#ifndef PHG_B2_PUSH_UNROLL
+#define PHG_B2_PUSH_UNROLL 1
+#endif
+constexpr int kB2PushUnroll = PHG_B2_PUSH_UNROLL;  // candidates per push-loop trip
+
 constexpr int kB2Round = 64;  // candidates drained per round: two per lane
 static_assert(kB2Round <= kH2Round, "the b2 rings reuse the h2 ring layout");
 
@@ -360,12 +365,17 @@ __global__ void __launch_bounds__(kH2Threads, 2)
                     uint32_t addr = ring + 2 * (pending + incl - n);
                     const uint32_t base3 = static_cast<uint32_t>((y0 + 3) * kH2RP + 16 + 8 * c);
                     uint32_t mm = R;
+                    // kB2PushUnroll items per loop trip (as in fused_h2_kernel's push)
                     while (mm) {
-                        uint32_t b;
-                        asm("bfind.u32 %0, %1;" : "=r"(b) : "r"(mm));
-                        mm ^= 1u << b;
-                        sts16(addr, base3 - (b & 3u) * kH2RP + (b >> 3) + (b & 4u));
-                        addr += 2;
+#pragma unroll
+                        for (int u = 0; u < kB2PushUnroll; ++u) {
+                            uint32_t b, m1;
+                            asm("bfind.u32 %0, %1;" : "=r"(b) : "r"(mm));
+                            asm("shl.b32 %0, 1, %1;" : "=r"(m1) : "r"(b));
+                            if (u == 0 || mm) sts16(addr + 2 * u, base3 - (b & 3u) * kH2RP + (b >> 3) + (b & 4u));
+                            mm ^= m1;
+                        }
+                        addr += 2 * kB2PushUnroll;
                     }
                     pending += total;
                     __syncwarp();
