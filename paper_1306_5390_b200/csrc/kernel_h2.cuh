@@ -424,8 +424,8 @@ __global__ void __launch_bounds__(kH2Threads, 2)
                         addr += 2 * kH2PushUnroll;
                     }
                     pending += total;
-                    __syncwarp();
                     if (pending >= kH2Round) {
+                        __syncwarp();  // other lanes' ring items are read only by a drain
                         int h = 0;
                         for (; pending - h >= kH2Round; h += kH2Round) drain(h, kH2Round);
                         pending -= h;

@@ -378,8 +378,8 @@ __global__ void __launch_bounds__(kH2Threads, 2)
                         addr += 2 * kB2PushUnroll;
                     }
                     pending += total;
-                    __syncwarp();
                     if (pending >= kB2Round) {
+                        __syncwarp();  // other lanes' ring items are read only by a drain
                         int h = 0;
                         for (; pending - h >= kB2Round; h += kB2Round) drain(h, kB2Round);
                         pending -= h;
