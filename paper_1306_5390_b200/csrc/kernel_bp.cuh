@@ -1,0 +1,461 @@
+// kernel_bp.cuh -- the beta = 1 hot path with packed-bit neighbour logic.
+//
+// fused_bp_kernel<T, ALE, WIDE>: T fused iterations of cardinality
+// (denoise.hpp:139-160) + removal (denoise.hpp:176-223) for beta = 1,
+// Faithful borders and card_threshold <= 3 (the reference defaults,
+// denoise.hpp:34-39).
+//
+// What decides a pixel.  With beta = 1, Faithful borders and thr <= 3 a pixel
+// is flagged iff it has at most thr-2 similar neighbours among its 8 in-bounds
+// neighbours (C = 1 + that count, C < thr), and a flagged pixel is replaced
+// iff its whole window is inside the image (an interior flagged pixel has
+// flag = 8 - #similar >= 7 > 9 - 3; a border pixel has flag <= in_bounds - 1
+// <= 5).  So the sweep only needs "at least one" / "at least two" similar
+// neighbours per pixel, which is bit-parallel logic once the similarity tests
+// are packed one bit per pixel.
+//
+// Sweep (one lane = a 32-px strip of a row, one warp = a 1024-px region row):
+//   - the four unordered pair directions E, S, SE, SW are tested in byte-SIMD
+//     (VABSDIFF4 + the carry trick of swar.cuh, 4 pairs per op), and each
+//     test's dissimilar bits are packed into one 32-bit word per 32 px
+//     (word i, byte j -> bit 8j + i: one shift-add per word);
+//   - a pair credits both of its pixels; credits to the eastern end are a
+//     one-pixel shift of the packed word (shE), the row below is carried in
+//     registers;
+//   - the 8 credits of a pixel are reduced to (o, w) = (>= 1 similar,
+//     >= 2 similar) with 3-input majority / or LOP3s: 32 pixels per op.
+//   Candidates are then a 32-bit word per strip row, stored in shared memory.
+// Replacement: each warp owns a band of rows; after the sweep its lanes split
+// the band's candidates evenly (a warp scan of the per-lane counts, each lane
+// takes a contiguous range of ceil(n/32)) and compute the exact RMS of the
+// dissimilar cells (byte-SIMD masks + IDP.4A sums, h2_rms).
+//
+// Band boundaries: a warp's first band row lacks the credits of the pairs with
+// the row above, which the warp above computes as the last step of its band;
+// it parks them in shared memory and the first row is finished after the
+// barrier that ends the sweep (warp 0 computes its own from the row above).
+//
+// Tiles.  Narrow images (width <= 512): a CTA holds two consecutive tiles
+// (image, row tile) side by side, one per half-warp (lanes 0-15 / 16-31),
+// each the full image width -- no column halo at all.  Wide images: one
+// 1024-px region per CTA, one column tile when width <= 1024, else 992 output
+// columns with 16-px aprons (TMA start coordinates are 16-byte aligned).
+// The image is staged once per launch by TMA, the T iterations ping-pong
+// between two shared buffers, and only the last iteration's owned rows go to
+// HBM (16-byte stores).
+//
+// Cells outside the image are masked out of every test (the reference's "out
+// of bounds cells are not in the window", denoise.hpp:145-149).
+#pragma once
+#include <cuda.h>
+#include <cstdint>
+
+#include "bp_launch.h"
+#include "kernel_h2.cuh"
+
+namespace phg {
+
+constexpr int kBpWarps = 8;
+constexpr int kBpThreads = 32 * kBpWarps;
+constexpr int kBpPad = 128;        // dynamic smem starts with a pad (window reads at region column -1)
+
+__host__ __device__ constexpr int bp_buf_bytes(int sh) { return (1024 * sh + 64 + 127) / 128 * 128; }
+__host__ __device__ constexpr int bp_smem_bytes(int sh) {
+    return kBpPad + 2 * bp_buf_bytes(sh) + sh * 32 * 4 + kBpWarps * 32 * 8;
+}
+
+
+// packed bit of strip pixel q (word q/4, byte q%4)
+__host__ __device__ constexpr uint32_t bp_bit(int q) { return 8u * static_cast<uint32_t>(q & 3) + (q >> 2); }
+// strip pixel of packed bit b
+__device__ __forceinline__ uint32_t bp_px(uint32_t b) { return 4u * (b & 7u) + (b >> 3); }
+
+// (a | b) & c and (a & b) & c as one opaque LOP3, so that the packing shift
+// below stays a shift-add (LEA.HI) instead of being split into SHF + LOP3
+__device__ __forceinline__ uint32_t lop_or_and(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t r;
+    asm("lop3.b32 %0, %1, %2, %3, 0xa8;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
+__device__ __forceinline__ uint32_t lop_and_and(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t r;
+    asm("lop3.b32 %0, %1, %2, %3, 0x80;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
+
+// dissimilar bits of the 32 pairs (a[i] byte j, b[i] byte j), packed:
+// VABSDIFF4, LOP3, IMAD (carry-trick add on the FMA pipe), LOP3, LEA.HI per word
+template <bool ALE>
+__device__ __forceinline__ uint32_t bp_dis(const uint32_t (&a)[8], const uint32_t (&b)[8], uint32_t k7,
+                                           uint32_t one) {
+    uint32_t acc = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const uint32_t d = __vabsdiffu4(a[i], b[i]);
+        const uint32_t t = (d & kLo7) * one + k7;
+        const uint32_t dis = ALE ? lop_or_and(d, t, kHi) : lop_and_and(d, t, kHi);
+        acc += dis >> (7 - i);
+    }
+    return acc;
+}
+
+// One pixel east: the bit of strip pixel q moves to pixel q+1; pixel 0 takes
+// pixel 31 of the lane to the west (lane 0 takes lane 31's, whose pixel 31
+// never has an eastern partner inside the region, so it is 0).
+__device__ __forceinline__ uint32_t bp_shE(uint32_t P, int west) {
+    const uint32_t prev = __shfl_sync(0xffffffffu, P, west);
+    return (P << 8) | ((P >> 23) & 0xfeu) | (prev >> 31);
+}
+
+__device__ __forceinline__ uint32_t maj3(uint32_t a, uint32_t b, uint32_t c) { return (a & b) | (c & (a | b)); }
+
+__device__ __forceinline__ uint4 lds128a(uint32_t a) {
+    uint4 v;
+    asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts128a(uint32_t a, uint4 v) {
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ void sts32a(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+// the lane's strip of one staged row: X[i] = pixels 4i..4i+3, EX[i] = pixels 4i+1..4i+4
+__device__ __forceinline__ void bp_load(uint32_t a, uint32_t (&X)[8], uint32_t (&EX)[8]) {
+    const uint4 u0 = lds128a(a), u1 = lds128a(a + 16);
+    const uint32_t nx = lds32a(a + 32);
+    X[0] = u0.x; X[1] = u0.y; X[2] = u0.z; X[3] = u0.w;
+    X[4] = u1.x; X[5] = u1.y; X[6] = u1.z; X[7] = u1.w;
+#pragma unroll
+    for (int i = 0; i < 7; ++i) EX[i] = __funnelshift_r(X[i], X[i + 1], 8);
+    EX[7] = __funnelshift_r(X[7], nx, 8);
+}
+
+// RMS replacement of one candidate (interior, Faithful, beta = 1), exactly as
+// removal_rows (denoise.hpp:199-217); `o1` = shared address of the window's
+// top-left cell, RP = staged row pitch.  Returns the new value.
+template <bool ALE, int RP>
+__device__ __forceinline__ uint32_t bp_replace(uint32_t o1, uint32_t k7) {
+    const uint32_t b4 = o1 & ~3u;
+    const uint32_t sel = 0x0210u + (o1 & 3u) * 0x0111u;  // bytes s, s+1, s+2
+    uint32_t R[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) R[r] = prmt(lds32a(b4 + r * RP), lds32a(b4 + r * RP + 4), sel);
+    const uint32_t n1 = prmt(R[0], R[1], 0x4210);  // t0 t1 t2 m0
+    const uint32_t n2 = prmt(R[1], R[2], 0x6542);  // m2 b0 b1 b2
+    const uint32_t p4 = prmt(R[1], 0, 0x1111);     // centre x4
+    const uint32_t d1 = __vabsdiffu4(n1, p4), d2 = __vabsdiffu4(n2, p4);
+    const uint32_t t1 = (d1 & kLo7) + k7, t2 = (d2 & kLo7) + k7;
+    const uint32_t dis1 = (ALE ? (d1 | t1) : (d1 & t1)) & kHi;
+    const uint32_t dis2 = (ALE ? (d2 | t2) : (d2 & t2)) & kHi;
+    const uint32_t f = __popc(dis1 | (dis2 >> 1));
+    const uint32_t S = __dp4a(n2 & msb_to_bytes(dis2), n2, __dp4a(n1 & msb_to_bytes(dis1), n1, 0u));
+    const float rcp = f == 8u ? 0.125f : 0.142857149f;  // f in {7, 8}
+    return h2_rms(S, f, rcp);
+}
+
+template <int T, bool ALE, bool WIDE>
+__global__ void __launch_bounds__(kBpThreads, 2)
+    fused_bp_kernel(const __grid_constant__ CUtensorMap src_map, const BpArgs a) {
+    static_assert(T >= 1 && T <= 8, "halo exceeds the aprons");
+    constexpr int HALO = T;
+    constexpr int RP = WIDE ? 1024 : 512;  // staged row pitch of one tile
+    constexpr int NH = WIDE ? 1 : 2;       // tiles per CTA
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    __shared__ uint64_t bar;
+    __shared__ unsigned int red[T][4];  // flagged h0, flagged h1, replaced h0, replaced h1
+
+    uint8_t* smem = smem_raw + kBpPad;
+    const int sh = a.th + 2 * HALO;
+    const int bufb = bp_buf_bytes(sh);
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+    const uint32_t s0 = smem_u32(smem);
+    const uint32_t cand_a = s0 + 2 * bufb;            // [sh][32] u32 candidate words
+    const uint32_t down_a = cand_a + sh * 32 * 4;     // [warps][32][2] u32 band-edge credits
+    const uint32_t half_bytes = static_cast<uint32_t>(sh) * 512u;  // narrow: tile B offset
+
+    // ---- the tiles of this CTA
+    const int per_img = a.tiles_x * a.tiles_y;
+    auto decode = [&](int t, int& img, int& x0, int& y0, int& out_rows) {
+        img = t / per_img;
+        const int r = t - img * per_img;
+        const int ty = r / a.tiles_x, tx = r - ty * a.tiles_x;
+        x0 = tx * a.x_step - a.x_apron;
+        const int out_r0 = (a.own_lo - a.row_base) + ty * a.th;
+        out_rows = min(a.th, (a.own_hi - a.row_base) - out_r0);
+        y0 = out_r0 - HALO;
+    };
+    const int tA = NH * blockIdx.x;
+    const int tB = tA + 1;
+    const bool hasB = !WIDE && tB < a.n_tiles;
+    int imgA, x0A, y0A, outA, imgB = 0, x0B = 0, y0B = 0, outB = 0;
+    decode(tA, imgA, x0A, y0A, outA);
+    if (hasB) decode(tB, imgB, x0B, y0B, outB);
+
+    // device early exit: an image whose previous iteration replaced nothing is
+    // at a fixed point (denoise.hpp:308); its iterations are plain copies
+    bool convA = false, convB = !hasB;
+    if (a.early && a.it0 > 0) {
+        convA = a.counters[(static_cast<int64_t>(imgA) * a.kcap + a.it0 - 1) * 2 + 1] == 0ull;
+        if (hasB) convB = a.counters[(static_cast<int64_t>(imgB) * a.kcap + a.it0 - 1) * 2 + 1] == 0ull;
+    }
+    const int nit = (convA && convB) ? 0 : T;
+
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        mbar_expect_tx(&bar, static_cast<uint32_t>(RP * sh * (hasB ? 2 : 1)));
+        tma_load_4d(smem, &src_map, 0, x0A / kChunk, y0A, imgA, &bar);
+        if (hasB) tma_load_4d(smem + half_bytes, &src_map, 0, x0B / kChunk, y0B, imgB, &bar);
+    }
+    if (tid < 4 * T) (&red[0][0])[tid] = 0;
+
+    // ---- per-lane constants: the lane's 32-px strip of its tile
+    const int half = WIDE ? 0 : (lane >> 4);
+    const int lw = WIDE ? lane : (lane & 15);
+    auto lbase = [&](int l) -> uint32_t {  // byte offset of lane l's strip in a buffer row 0
+        return WIDE ? static_cast<uint32_t>(l) * 32u
+                    : static_cast<uint32_t>(l >> 4) * half_bytes + static_cast<uint32_t>(l & 15) * 32u;
+    };
+    const uint32_t cb = lbase(lane);
+    const bool myhas = half ? hasB : true;
+    const int myx0 = half ? x0B : x0A;
+    const int gy0 = a.row_base + (half ? y0B : y0A);
+    const int myout = half ? outB : outA;
+    const bool myconv = half ? convB : convA;
+    const int W = a.width, H = a.height;
+    uint32_t cIn = 0, cE = 0, cInt = 0, cOwn = 0;
+#pragma unroll 4
+    for (int q = 0; q < 32; ++q) {
+        const int rc = lw * 32 + q;
+        const int gx = myx0 + rc;
+        const bool in = myhas && gx >= 0 && gx < W;
+        const bool in1 = myhas && rc + 1 < RP && gx + 1 >= 0 && gx + 1 < W;
+        const uint32_t bit = 1u << bp_bit(q);
+        if (in) cIn |= bit;
+        if (in && in1) cE |= bit;
+        if (myhas && gx >= 1 && gx < W - 1) cInt |= bit;
+        const bool own_col = !WIDE || (rc >= a.x_apron && rc < a.x_apron + a.x_step);
+        if (in && own_col) cOwn |= bit;
+    }
+    const uint32_t cF = myconv ? 0u : (cIn & a.enable);
+    // row classes (buffer rows): valid [vlo, vhi), interior [ilo, ihi), owned [HALO, HALO + myout)
+    const int vlo = myhas ? max(0, -gy0) : 0;
+    const int vhi = myhas ? max(vlo, min(sh, H - gy0)) : 0;
+    const int ilo = max(0, 1 - gy0);
+    const int ihi = myhas ? max(ilo, min(sh, H - 1 - gy0)) : ilo;
+    auto rowin = [&](int y) { return static_cast<unsigned>(y - vlo) < static_cast<unsigned>(vhi - vlo); };
+    auto rowint = [&](int y) { return static_cast<unsigned>(y - ilo) < static_cast<unsigned>(ihi - ilo); };
+    auto rowown = [&](int y) { return static_cast<unsigned>(y - HALO) < static_cast<unsigned>(myout); };
+    const int west = (lane + 31) & 31;
+
+    __syncthreads();  // barrier init + counters visible
+    mbar_wait(&bar, 0);
+
+    for (int t = 0; t < nit; ++t) {
+        const uint32_t src = s0 + ((t & 1) ? bufb : 0);
+        const uint32_t dst = s0 + ((t & 1) ? 0 : bufb);
+        const int lo = t + 1, n = sh - 2 - 2 * t;  // computed rows [lo, lo + n)
+        const int nb = min(kBpWarps, n);
+        const int b0 = lo + n * warp / nb, b1 = lo + n * (warp + 1) / nb;
+        const bool active = warp < nb;
+        unsigned fl = 0, rp = 0;  // owned flagged / replaced (this lane's strip)
+        unsigned cnt = 0;         // candidates in this lane's strip over the band
+        uint32_t of = 0, wf = 0;  // the band's first row before its upper credits
+        uint32_t oM = 0, wM = 0;  // warp 0: the first row's upper credits
+
+        auto finalize = [&](int y, uint32_t o, uint32_t w) {
+            const uint32_t F = ~(w | (o & a.sel2)) & (rowin(y) ? cF : 0u);
+            const uint32_t R = F & (rowint(y) ? cInt : 0u);
+            if (rowown(y)) {
+                fl += __popc(F & cOwn);
+                rp += __popc(R & cOwn);
+            }
+            sts32a(cand_a + (y * 32 + lane) * 4, R);
+            cnt += __popc(R);
+        };
+
+        if (active) {
+            uint32_t X[8], EX[8], Xn[8], EXn[8];
+            bp_load(src + cb + b0 * RP, X, EX);
+            bool rv = rowin(b0);
+            uint32_t e = ~bp_dis<ALE>(X, EX, a.k7, a.one) & (rv ? cE : 0u);
+            uint32_t oP = 0, wP = 0, seP = 0;  // pairs with the row above: s|sw, s&sw, se
+            if (warp == 0) {  // the row above the computed range is staged: credits from it
+                bp_load(src + cb + (b0 - 1) * RP, Xn, EXn);
+                const bool rp_ = rowin(b0 - 1) && rv;
+                const uint32_t s_ = ~bp_dis<ALE>(Xn, X, a.k7, a.one) & (rp_ ? cIn : 0u);
+                const uint32_t se_ = ~bp_dis<ALE>(Xn, EX, a.k7, a.one) & (rp_ ? cE : 0u);
+                const uint32_t sw_ = ~bp_dis<ALE>(EXn, X, a.k7, a.one) & (rp_ ? cE : 0u);
+                const uint32_t sse = bp_shE(se_, west);
+                oM = s_ | sw_ | sse;
+                wM = maj3(s_, sw_, sse);
+            }
+            for (int y = b0; y < b1; ++y) {
+                bp_load(src + cb + (y + 1) * RP, Xn, EXn);
+                const bool rvn = rowin(y + 1);
+                const bool both = rv && rvn;
+                const uint32_t s = ~bp_dis<ALE>(X, Xn, a.k7, a.one) & (both ? cIn : 0u);
+                const uint32_t se = ~bp_dis<ALE>(X, EXn, a.k7, a.one) & (both ? cE : 0u);
+                const uint32_t sw = ~bp_dis<ALE>(EX, Xn, a.k7, a.one) & (both ? cE : 0u);
+                // unshifted credits of row y: s(y-1), sw(y-1) [oP, wP], e, s, se
+                const uint32_t o2 = e | s | se, w2 = maj3(e, s, se);
+                const uint32_t wA = wP | w2 | (oP & o2), oA = oP | o2;
+                // credits to the eastern end: e(y), se(y-1), sw(y)
+                const uint32_t oB = bp_shE(e | seP | sw, west);
+                const uint32_t wB = bp_shE(maj3(e, seP, sw), west);
+                const uint32_t w = wA | wB | (oA & oB), o = oA | oB;
+                if (y == b0) {
+                    of = o;
+                    wf = w;
+                } else {
+                    finalize(y, o, w);
+                }
+                // the unchanged row goes to the destination (candidates are
+                // overwritten by the replacement pass)
+                const uint32_t da = dst + cb + y * RP;
+                sts128a(da, make_uint4(X[0], X[1], X[2], X[3]));
+                sts128a(da + 16, make_uint4(X[4], X[5], X[6], X[7]));
+                oP = s | sw;
+                wP = s & sw;
+                seP = se;
+                if (y + 1 < b1) e = ~bp_dis<ALE>(Xn, EXn, a.k7, a.one) & (rvn ? cE : 0u);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    X[i] = Xn[i];
+                    EX[i] = EXn[i];
+                }
+                rv = rvn;
+            }
+            // credits of the pairs (b1-1, b1) for the next band's first row
+            if (warp + 1 < nb) {
+                const uint32_t sse = bp_shE(seP, west);
+                const uint32_t dn = down_a + (warp * 32 + lane) * 8;
+                sts32a(dn, oP | sse);
+                sts32a(dn + 4, wP | (oP & sse));  // maj3(s, sw, sse)
+            }
+        }
+        __syncthreads();  // the band edges are in place; dst rows of every band copied
+        if (active) {
+            if (warp > 0) {
+                const uint32_t dn = down_a + ((warp - 1) * 32 + lane) * 8;
+                oM = lds32a(dn);
+                wM = lds32a(dn + 4);
+            }
+            finalize(b0, of | oM, wf | wM | (of & oM));
+            __syncwarp();
+            // ---- replacement of the band's candidates, split evenly over the lanes
+            unsigned incl = cnt;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const unsigned v = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lane >= d) incl += v;
+            }
+            const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
+            if (total) {
+                const unsigned q = (total + 31) >> 5;
+                const unsigned s = lane * q;
+                const unsigned e = min(total, s + q);
+                // owner lane of candidate s: the first lane whose inclusive count exceeds s
+                int ol = 0;
+#pragma unroll
+                for (int step = 16; step; step >>= 1) {
+                    const unsigned v = __shfl_sync(0xffffffffu, incl, ol + step - 1);
+                    if (v <= s) ol += step;
+                }
+                const unsigned excl = __shfl_sync(0xffffffffu, incl - cnt, ol);
+                int row = b0, col = min(ol, 31);
+                uint32_t w = 0;
+                if (s < e) {
+                    unsigned skip = s - excl;
+                    w = lds32a(cand_a + (row * 32 + col) * 4);
+                    while (skip >= static_cast<unsigned>(__popc(w))) {
+                        skip -= __popc(w);
+                        ++row;
+                        w = lds32a(cand_a + (row * 32 + col) * 4);
+                    }
+                    for (; skip; --skip) w ^= 1u << (31 - __clz(w));
+                }
+                // next candidate in (column, row) order: returns the window corner
+                auto pop = [&](uint32_t& dsta) -> uint32_t {
+                    while (w == 0) {
+                        if (++row == b1) {
+                            row = b0;
+                            ++col;
+                        }
+                        w = lds32a(cand_a + (row * 32 + col) * 4);
+                    }
+                    const uint32_t b = 31 - __clz(w);
+                    w ^= 1u << b;
+                    const uint32_t off = lbase(col) + static_cast<uint32_t>(row) * RP + bp_px(b);
+                    dsta = dst + off;
+                    return src + off - RP - 1;
+                };
+                const unsigned my = e > s ? e - s : 0u;
+                for (unsigned k = 0; k < my; k += 2) {
+                    uint32_t d0, d1 = 0;
+                    const uint32_t c0 = pop(d0);
+                    const bool two = k + 1 < my;
+                    uint32_t c1 = c0;
+                    if (two) c1 = pop(d1);
+                    const uint32_t v0 = bp_replace<ALE, RP>(c0, a.k7);
+                    const uint32_t v1 = bp_replace<ALE, RP>(c1, a.k7);
+                    sts8a(d0, v0);
+                    if (two) sts8a(d1, v1);
+                }
+            }
+        }
+        // per-tile counters of this iteration
+        unsigned flA = (WIDE || lane < 16) ? fl : 0u, flB = fl - flA;
+        unsigned rpA = (WIDE || lane < 16) ? rp : 0u, rpB = rp - rpA;
+        flA = __reduce_add_sync(0xffffffffu, flA);
+        rpA = __reduce_add_sync(0xffffffffu, rpA);
+        if (!WIDE) {
+            flB = __reduce_add_sync(0xffffffffu, flB);
+            rpB = __reduce_add_sync(0xffffffffu, rpB);
+        }
+        if (lane == 0) {
+            if (flA) atomicAdd(&red[t][0], flA);
+            if (flB) atomicAdd(&red[t][1], flB);
+            if (rpA) atomicAdd(&red[t][2], rpA);
+            if (rpB) atomicAdd(&red[t][3], rpB);
+        }
+        __syncthreads();
+    }
+
+    // ---- owned output rows: 16-byte coalesced stores
+    {
+        const uint8_t* fin = smem + ((nit & 1) ? bufb : 0);
+        constexpr int kChunksRow = RP / 16;
+        const int c_lo = a.x_apron / 16;
+        const int c_n = WIDE ? a.x_step / 16 : kChunksRow;
+        const int rows = max(outA, outB);
+        for (int i = tid; i < NH * rows * c_n; i += kBpThreads) {
+            const int hh = WIDE ? 0 : i / (rows * c_n);
+            const int rem = i - hh * rows * c_n;
+            const int r = rem / c_n, ch = c_lo + rem - r * c_n;
+            const int out_h = hh ? outB : outA;
+            const int x0h = hh ? x0B : x0A;
+            if (r >= out_h || x0h + 16 * ch >= a.width) continue;
+            const int y = HALO + r;
+            const uint4 v = *reinterpret_cast<const uint4*>(fin + hh * half_bytes + y * RP + 16 * ch);
+            const int imgh = hh ? imgB : imgA;
+            const int y0h = hh ? y0B : y0A;
+            *reinterpret_cast<uint4*>(a.dst + imgh * a.image_stride + static_cast<int64_t>(y0h + y) * a.pitch +
+                                      x0h + 16 * ch) = v;
+            mirror_row16(a.peers, a.row_base + y0h + y, a.pitch, x0h + 16 * ch, v);
+        }
+    }
+    if (tid < 4 * T && nit > 0) {
+        const int t = tid >> 2, which = tid & 3;
+        const unsigned v = red[t][which];
+        const int img = (which & 1) ? imgB : imgA;
+        if (v) atomicAdd(&a.counters[(static_cast<int64_t>(img) * a.kcap + a.it0 + t) * 2 + (which >> 1)],
+                         static_cast<unsigned long long>(v));
+    }
+}
+
+}  // namespace phg

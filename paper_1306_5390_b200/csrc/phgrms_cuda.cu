@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "../../include/phgrms_b200.h"
+#include "bp_launch.h"
 #include "kernel_card.cuh"
 #include "kernel_gen.cuh"
 #include "kernel_h2.cuh"
@@ -90,7 +91,7 @@ std::once_flag g_encode_once;
 
 // The image is viewed as [images][rows][chunks][16 px] so that one 4-D box
 // {16, 33, SH, 1} lands as a dense [SH][528] shared tile (kernels.cuh).
-int encode_map(CUtensorMap* map, const phg_dev_image& im, int box_rows) {
+int encode_map(CUtensorMap* map, const phg_dev_image& im, int box_rows, int box_chunks = phg::kChunks) {
     std::call_once(g_encode_once, [] {
         cudaDriverEntryPointQueryResult q;
         void* fn = nullptr;
@@ -109,7 +110,7 @@ int encode_map(CUtensorMap* map, const phg_dev_image& im, int box_rows) {
     cuuint64_t strides[3] = {16, static_cast<cuuint64_t>(im.pitch),
                              static_cast<cuuint64_t>(im.n_images > 1 ? im.image_stride
                                                                      : im.pitch * im.rows)};
-    cuuint32_t box[4] = {16, static_cast<cuuint32_t>(phg::kChunks), static_cast<cuuint32_t>(box_rows), 1};
+    cuuint32_t box[4] = {16, static_cast<cuuint32_t>(box_chunks), static_cast<cuuint32_t>(box_rows), 1};
     cuuint32_t estr[4] = {1, 1, 1, 1};
     CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, im.data, dims, strides, box, estr,
                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -166,7 +167,7 @@ Launch plan_rows(int own_rows, int halo, int rows_target) {
 // ceil(CTAs / resident CTAs) waves of near-equal CTAs, each sweeping
 // T*sh - T(T+1) rows, so small grids (one 4K image = 240 CTAs of 36 rows on
 // 296 slots) pick the tile height that minimises waves x rows per CTA.
-Launch plan_rows_h2(int own_rows, int halo, int rows_target, int n_images, int tiles_x) {
+Launch plan_rows_h2(int own_rows, int halo, int rows_target, int n_images, int tiles_x, int per_cta = 2) {
     static const int slots = [] {
         int dev = 0, sms = 148;
         if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -177,7 +178,7 @@ Launch plan_rows_h2(int own_rows, int halo, int rows_target, int n_images, int t
     double best_cost = 1e300;
     for (int th = std::min(th_max, own_rows); th >= std::max(1, std::min(4, own_rows)); --th) {
         const int64_t tiles_y = (own_rows + th - 1) / th;
-        const int64_t ctas = (static_cast<int64_t>(n_images) * tiles_x * tiles_y + 1) / 2;
+        const int64_t ctas = (static_cast<int64_t>(n_images) * tiles_x * tiles_y + per_cta - 1) / per_cta;
         const int64_t waves = (ctas + slots - 1) / slots;
         const int sh = th + 2 * halo;
         const double cost = static_cast<double>(waves) * (halo * sh - halo * (halo + 1) + 8);
@@ -303,6 +304,80 @@ int launch_h2(const phg_dev_image& src, const phg_dev_image& dst, int row_base, 
     return PHG_OK;
 }
 
+// The packed-bit kernel (kernel_bp.cuh) runs beta = 1, Faithful borders,
+// card_threshold <= 3 -- the reference defaults (PHG_NO_BP=1 falls back to
+// the fp16 two-tile kernel).
+bool use_bp(const phg_params& p, int iters) {
+    static const bool off = getenv("PHG_NO_BP") != nullptr;
+    return !off && p.beta == 1 && p.border == PHG_BORDER_FAITHFUL && p.card_threshold <= 3 && iters <= 5;
+}
+
+// staged rows per tile (tunable: PHG_BP_ROWS); 48 keeps two CTAs per SM
+int bp_rows_target() {
+    static const int v = [] {
+        const char* e = getenv("PHG_BP_ROWS");
+        return e ? std::max(8, std::min(phg::kBpMaxRows, atoi(e))) : 48;
+    }();
+    return v;
+}
+
+// Column tiling of the packed-bit kernel: images up to 512 px wide put two
+// full-width tiles in one CTA; up to 1024 px one full-width tile; wider ones
+// 992 output columns per tile with 16-px aprons.
+struct BpCols {
+    bool wide;
+    int tiles_x, x_step, x_apron;
+};
+BpCols bp_cols(int width) {
+    if (width <= 512) return {false, 1, 512, 0};
+    if (width <= 1024) return {true, 1, 1024, 0};
+    return {true, (width + 991) / 992, 992, 16};
+}
+
+int launch_bp(const phg_dev_image& src, const phg_dev_image& dst, int row_base, int height, int own_lo,
+              int own_hi, const phg_params& p, int it0, int iters, uint64_t* counters, int kcap,
+              cudaStream_t stream, const phg::HaloPeers& peers, bool early) {
+    const int halo = iters;
+    const BpCols cols = bp_cols(src.width);
+    const Launch L = plan_rows_h2(own_hi - own_lo, halo, bp_rows_target(), src.n_images, cols.tiles_x,
+                                  cols.wide ? 1 : 2);
+    const int sh = L.th + 2 * halo;
+    if (sh > phg::kBpMaxRows) return fail(PHG_EINVAL, "tile too tall");
+    const size_t smem = phg::bp_smem(sh);
+    CUtensorMap map;
+    PHG_TRY(encode_map(&map, src, sh, cols.wide ? 64 : 32));
+    phg::BpArgs a{};
+    a.dst = dst.data;
+    a.pitch = dst.pitch;
+    a.image_stride = dst.image_stride;
+    a.width = src.width;
+    a.height = height;
+    a.row_base = row_base;
+    a.own_lo = own_lo;
+    a.own_hi = own_hi;
+    a.th = L.th;
+    a.tiles_x = cols.tiles_x;
+    a.tiles_y = L.tiles_y;
+    const int64_t n_tiles = static_cast<int64_t>(src.n_images) * a.tiles_x * a.tiles_y;
+    if (n_tiles > (int64_t(1) << 31) - 2) return fail(PHG_EINVAL, "too many tiles for one launch");
+    a.n_tiles = static_cast<int>(n_tiles);
+    a.x_step = cols.x_step;
+    a.x_apron = cols.x_apron;
+    a.k7 = ((256u - static_cast<uint32_t>(p.alpha)) & 0x7fu) * 0x01010101u;
+    a.one = 1u;
+    a.sel2 = p.card_threshold == 2 ? ~0u : 0u;
+    a.enable = p.card_threshold >= 2 ? ~0u : 0u;
+    a.it0 = it0;
+    a.kcap = kcap;
+    a.early = early ? 1 : 0;
+    a.counters = reinterpret_cast<unsigned long long*>(counters);
+    a.peers = peers;
+    const unsigned grid = static_cast<unsigned>(cols.wide ? n_tiles : (n_tiles + 1) / 2);
+    PHG_CUDA(phg::launch_bp_kernel(iters, p.alpha <= 128, cols.wide, map, a, grid, smem, stream));
+    ++g_launches;
+    return PHG_OK;
+}
+
 // beta = 1 cardinality map (kCardMap) or C < thr count (kCardCount) over
 // whole images (rows = src.rows), fp16 two-tile sweep (kernel_card.cuh).
 int launch_card_h2(const phg_dev_image& src, int alpha, int mode, int thr, int32_t* card, int64_t card_pitch,
@@ -406,7 +481,11 @@ int launch_card_tb(const phg_dev_image& src, int alpha, int beta, int32_t* card,
 
 int launch_fused(const phg_dev_image& src, const phg_dev_image& dst, int row_base, int height,
                  int own_lo, int own_hi, const phg_params& p, int it0, int iters,
-                 uint64_t* counters, int kcap, cudaStream_t stream, const phg::HaloPeers& peers = kNoPeers) {
+                 uint64_t* counters, int kcap, cudaStream_t stream, const phg::HaloPeers& peers = kNoPeers,
+                 bool early = false) {
+    if (use_bp(p, iters))
+        return launch_bp(src, dst, row_base, height, own_lo, own_hi, p, it0, iters, counters, kcap, stream, peers,
+                         early);
     if (use_h2(p, iters))
         return launch_h2(src, dst, row_base, height, own_lo, own_hi, p, it0, iters, counters, kcap, stream,
                          peers);
@@ -523,10 +602,10 @@ int launch_scalar(int mode, const phg_dev_image& src, const phg_dev_image* dst,
 // available, else one scalar fused launch per iteration (iters must be 1).
 int step(const phg_dev_image& src, const phg_dev_image& dst, int row_base, int height, int own_lo,
          int own_hi, const phg_params& p, int it0, int iters, uint64_t* counters, int kcap,
-         cudaStream_t stream, const phg::HaloPeers& peers = kNoPeers) {
+         cudaStream_t stream, const phg::HaloPeers& peers = kNoPeers, bool early = false) {
     if (max_fused(p.beta) > 0)
         return launch_fused(src, dst, row_base, height, own_lo, own_hi, p, it0, iters, counters,
-                            kcap, stream, peers);
+                            kcap, stream, peers, early);
     if (iters != 1) return fail(PHG_EINVAL, "beta >= 3 runs one iteration per launch");
     return launch_scalar(phg::kModeFused, src, &dst, nullptr, nullptr, 0, row_base, height, own_lo,
                          own_hi, p, it0, counters, kcap, stream, peers);
@@ -836,6 +915,9 @@ const char* phg_fused_kernel_name(const phg_params* p, int iters) {
     if (iters > max_fused(p->beta)) return "";
     static const char* const h2b2[] = {"", "fused_h2b2_kernel<T=1>", "fused_h2b2_kernel<T=2>",
                                        "fused_h2b2_kernel<T=3>", "fused_h2b2_kernel<T=4>"};
+    static const char* const bp[] = {"", "fused_bp_kernel<T=1>", "fused_bp_kernel<T=2>", "fused_bp_kernel<T=3>",
+                                     "fused_bp_kernel<T=4>", "fused_bp_kernel<T=5>"};
+    if (use_bp(*p, iters)) return bp[iters];
     if (use_h2(*p, iters)) return h2[iters];
     if (use_h2b2(*p, iters)) return h2b2[iters];
     return p->beta == 1 ? b1[iters] : p->beta == 2 ? b2[iters] : b3[iters];
@@ -953,7 +1035,9 @@ int phg_dev_denoise(const phg_dev_image* src, const phg_dev_image* dst, const ph
     int it0 = 0;
     for (int i = 0; i < nl; ++i) {
         const phg_dev_image* out = ((nl - 1 - i) % 2 == 0) ? dst : tmp;
-        PHG_TRY(step(*cur, *out, 0, src->rows, 0, src->rows, *p, it0, plan[i], counters, k, st));
+        // whole images: the counters of the previous launch are complete, so
+        // converged images skip their iterations (early exit, kernel_bp.cuh)
+        PHG_TRY(step(*cur, *out, 0, src->rows, 0, src->rows, *p, it0, plan[i], counters, k, st, kNoPeers, true));
         cur = out;
         it0 += plan[i];
     }
