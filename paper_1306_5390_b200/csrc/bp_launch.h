@@ -10,7 +10,7 @@
 
 namespace phg {
 
-constexpr int kBpMaxRows = 52;  // staged rows: two CTAs per SM
+constexpr int kBpMaxRows = 46;  // staged rows: two CTAs per SM
 
 struct BpArgs {
     uint8_t* dst;

@@ -58,10 +58,12 @@ namespace phg {
 constexpr int kBpWarps = 8;
 constexpr int kBpThreads = 32 * kBpWarps;
 constexpr int kBpPad = 128;        // dynamic smem starts with a pad (window reads at region column -1)
+constexpr int kBpList = 64 + 1024;  // per-warp candidate list (u16 items): < one round + one row
 
 __host__ __device__ constexpr int bp_buf_bytes(int sh) { return (1024 * sh + 64 + 127) / 128 * 128; }
+// pad, two staged buffers, band-edge credits [warps][32][2], candidate lists [warps][kBpList]
 __host__ __device__ constexpr int bp_smem_bytes(int sh) {
-    return kBpPad + 2 * bp_buf_bytes(sh) + sh * 32 * 4 + kBpWarps * 32 * 8;
+    return kBpPad + 2 * bp_buf_bytes(sh) + kBpWarps * 32 * 8 + kBpWarps * kBpList * 2;
 }
 
 
@@ -69,6 +71,20 @@ __host__ __device__ constexpr int bp_smem_bytes(int sh) {
 __host__ __device__ constexpr uint32_t bp_bit(int q) { return 8u * static_cast<uint32_t>(q & 3) + (q >> 2); }
 // strip pixel of packed bit b
 __device__ __forceinline__ uint32_t bp_px(uint32_t b) { return 4u * (b & 7u) + (b >> 3); }
+
+// packed mask of the strip pixels q in [lo, hi) (clamped to [0, 32)): byte j
+// holds pixels 4i + j, i.e. bits i in [ceil((lo-j)/4), ceil((hi-j)/4))
+__device__ __forceinline__ uint32_t bp_range(int lo, int hi) {
+    lo = max(lo, 0);
+    hi = min(hi, 32);
+    uint32_t m = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int il = (lo - j + 3) >> 2, ih = max(il, (hi - j + 3) >> 2);
+        m |= (((1u << ih) - 1u) & ~((1u << il) - 1u)) << (8 * j);
+    }
+    return m;
+}
 
 // (a | b) & c and (a & b) & c as one opaque LOP3, so that the packing shift
 // below stays a shift-add (LEA.HI) instead of being split into SHF + LOP3
@@ -174,8 +190,8 @@ __global__ void __launch_bounds__(kBpThreads, 2)
     const int lane = tid & 31;
     const int warp = tid >> 5;
     const uint32_t s0 = smem_u32(smem);
-    const uint32_t cand_a = s0 + 2 * bufb;            // [sh][32] u32 candidate words
-    const uint32_t down_a = cand_a + sh * 32 * 4;     // [warps][32][2] u32 band-edge credits
+    const uint32_t down_a = s0 + 2 * bufb;            // [warps][32][2] u32 band-edge credits
+    const uint32_t list_a = down_a + kBpWarps * 32 * 8 + warp * kBpList * 2;  // this warp's u16 list
     const uint32_t half_bytes = static_cast<uint32_t>(sh) * 512u;  // narrow: tile B offset
 
     // ---- the tiles of this CTA
@@ -227,20 +243,15 @@ __global__ void __launch_bounds__(kBpThreads, 2)
     const int myout = half ? outB : outA;
     const bool myconv = half ? convB : convA;
     const int W = a.width, H = a.height;
-    uint32_t cIn = 0, cE = 0, cInt = 0, cOwn = 0;
-#pragma unroll 4
-    for (int q = 0; q < 32; ++q) {
-        const int rc = lw * 32 + q;
-        const int gx = myx0 + rc;
-        const bool in = myhas && gx >= 0 && gx < W;
-        const bool in1 = myhas && rc + 1 < RP && gx + 1 >= 0 && gx + 1 < W;
-        const uint32_t bit = 1u << bp_bit(q);
-        if (in) cIn |= bit;
-        if (in && in1) cE |= bit;
-        if (myhas && gx >= 1 && gx < W - 1) cInt |= bit;
-        const bool own_col = !WIDE || (rc >= a.x_apron && rc < a.x_apron + a.x_step);
-        if (in && own_col) cOwn |= bit;
-    }
+    // column classes of the strip (packed masks): in the image, E pair inside
+    // the image and the region, interior (whole window in the image), output
+    const int gxs = myx0 + lw * 32;  // global column of strip pixel 0
+    const int wr = max(min(W - gxs, 64), -64);  // clamped distances keep the ints small
+    const int gl = max(min(-gxs, 64), -64);
+    const uint32_t cIn = myhas ? bp_range(gl, wr) : 0u;
+    const uint32_t cE = myhas ? bp_range(gl, min(wr - 1, RP - 1 - lw * 32)) : 0u;
+    const uint32_t cInt = myhas ? bp_range(gl + 1, wr - 1) : 0u;
+    const uint32_t cOwn = WIDE ? (cIn & bp_range(a.x_apron - lw * 32, a.x_apron + a.x_step - lw * 32)) : cIn;
     const uint32_t cF = myconv ? 0u : (cIn & a.enable);
     // row classes (buffer rows): valid [vlo, vhi), interior [ilo, ihi), owned [HALO, HALO + myout)
     const int vlo = myhas ? max(0, -gy0) : 0;
@@ -263,10 +274,10 @@ __global__ void __launch_bounds__(kBpThreads, 2)
         const int b0 = lo + n * warp / nb, b1 = lo + n * (warp + 1) / nb;
         const bool active = warp < nb;
         unsigned fl = 0, rp = 0;  // owned flagged / replaced (this lane's strip)
-        unsigned cnt = 0;         // candidates in this lane's strip over the band
         uint32_t of = 0, wf = 0;  // the band's first row before its upper credits
         uint32_t oM = 0, wM = 0;  // warp 0: the first row's upper credits
 
+        // flagged (F) and replaced (R) pixels of row y from its (o, w) counts
         auto finalize = [&](int y, uint32_t o, uint32_t w) {
             const uint32_t F = ~(w | (o & a.sel2)) & (rowin(y) ? cF : 0u);
             const uint32_t R = F & (rowint(y) ? cInt : 0u);
@@ -274,8 +285,61 @@ __global__ void __launch_bounds__(kBpThreads, 2)
                 fl += __popc(F & cOwn);
                 rp += __popc(R & cOwn);
             }
-            sts32a(cand_a + (y * 32 + lane) * 4, R);
-            cnt += __popc(R);
+            return R;
+        };
+        unsigned pending = 0;  // warp-uniform: candidates waiting at list[0, pending)
+        // replaces the candidates list[h, h + n), n <= 64: two per lane, loads first
+        auto drain = [&](unsigned h, unsigned n) {
+            const bool a0 = lane < n, a1 = lane + 32 < n;
+            const uint32_t o0 = lds16(list_a + 2 * (h + (a0 ? lane : 0u)));
+            const uint32_t o1 = lds16(list_a + 2 * (h + (a1 ? lane + 32u : 0u)));
+            const uint32_t v0 = bp_replace<ALE, RP>(src + o0 - RP - 1, a.k7);
+            const uint32_t v1 = bp_replace<ALE, RP>(src + o1 - RP - 1, a.k7);
+            if (a0) sts8a(dst + o0, v0);
+            if (a1) sts8a(dst + o1, v1);
+        };
+        // appends row y's candidates R (u16 buffer offsets) at the lane's prefix
+        // in the warp list, three per loop trip; drains whole rounds of 64
+        auto push = [&](uint32_t R, int y) {
+            const unsigned c = __popc(R);
+            unsigned incl = c;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const unsigned v = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lane >= d) incl += v;
+            }
+            const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
+            if (total == 0) return;
+            uint32_t la = list_a + 2 * (pending + incl - c);
+            const uint32_t rowoff = cb + static_cast<uint32_t>(y) * RP;
+            uint32_t mm = R;
+            while (mm) {
+#pragma unroll
+                for (int u = 0; u < 3; ++u) {
+                    uint32_t b, m1;
+                    asm("bfind.u32 %0, %1;" : "=r"(b) : "r"(mm));    // ~0 once mm is empty
+                    asm("shl.b32 %0, 1, %1;" : "=r"(m1) : "r"(b));   // 0 for shifts >= 32
+                    if (u == 0 || mm) sts16(la + 2 * u, rowoff + bp_px(b));
+                    mm ^= m1;
+                }
+                la += 6;
+            }
+            pending += total;
+            if (pending >= 64) {
+                __syncwarp();  // items and the destination row copies are visible
+                unsigned h = 0;
+                for (; pending - h >= 64; h += 64) drain(h, 64);
+                pending -= h;
+                __syncwarp();
+                if (pending) {  // the leftovers (< 64) move to the front
+                    const uint32_t l0 = lane < pending ? lds16(list_a + 2 * (h + lane)) : 0u;
+                    const uint32_t l1 = lane + 32 < pending ? lds16(list_a + 2 * (h + lane + 32)) : 0u;
+                    __syncwarp();
+                    if (lane < pending) sts16(list_a + 2 * lane, l0);
+                    if (lane + 32 < pending) sts16(list_a + 2 * (lane + 32), l1);
+                }
+                __syncwarp();
+            }
         };
 
         if (active) {
@@ -294,6 +358,7 @@ __global__ void __launch_bounds__(kBpThreads, 2)
                 oM = s_ | sw_ | sse;
                 wM = maj3(s_, sw_, sse);
             }
+#pragma unroll 2
             for (int y = b0; y < b1; ++y) {
                 bp_load(src + cb + (y + 1) * RP, Xn, EXn);
                 const bool rvn = rowin(y + 1);
@@ -308,17 +373,17 @@ __global__ void __launch_bounds__(kBpThreads, 2)
                 const uint32_t oB = bp_shE(e | seP | sw, west);
                 const uint32_t wB = bp_shE(maj3(e, seP, sw), west);
                 const uint32_t w = wA | wB | (oA & oB), o = oA | oB;
+                // the unchanged row goes to the destination (candidates are
+                // overwritten by the replacement)
+                const uint32_t da = dst + cb + y * RP;
+                sts128a(da, make_uint4(X[0], X[1], X[2], X[3]));
+                sts128a(da + 16, make_uint4(X[4], X[5], X[6], X[7]));
                 if (y == b0) {
                     of = o;
                     wf = w;
                 } else {
-                    finalize(y, o, w);
+                    push(finalize(y, o, w), y);
                 }
-                // the unchanged row goes to the destination (candidates are
-                // overwritten by the replacement pass)
-                const uint32_t da = dst + cb + y * RP;
-                sts128a(da, make_uint4(X[0], X[1], X[2], X[3]));
-                sts128a(da + 16, make_uint4(X[4], X[5], X[6], X[7]));
                 oP = s | sw;
                 wP = s & sw;
                 seP = se;
@@ -345,67 +410,10 @@ __global__ void __launch_bounds__(kBpThreads, 2)
                 oM = lds32a(dn);
                 wM = lds32a(dn + 4);
             }
-            finalize(b0, of | oM, wf | wM | (of & oM));
-            __syncwarp();
-            // ---- replacement of the band's candidates, split evenly over the lanes
-            unsigned incl = cnt;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const unsigned v = __shfl_up_sync(0xffffffffu, incl, d);
-                if (lane >= d) incl += v;
-            }
-            const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
-            if (total) {
-                const unsigned q = (total + 31) >> 5;
-                const unsigned s = lane * q;
-                const unsigned e = min(total, s + q);
-                // owner lane of candidate s: the first lane whose inclusive count exceeds s
-                int ol = 0;
-#pragma unroll
-                for (int step = 16; step; step >>= 1) {
-                    const unsigned v = __shfl_sync(0xffffffffu, incl, ol + step - 1);
-                    if (v <= s) ol += step;
-                }
-                const unsigned excl = __shfl_sync(0xffffffffu, incl - cnt, ol);
-                int row = b0, col = min(ol, 31);
-                uint32_t w = 0;
-                if (s < e) {
-                    unsigned skip = s - excl;
-                    w = lds32a(cand_a + (row * 32 + col) * 4);
-                    while (skip >= static_cast<unsigned>(__popc(w))) {
-                        skip -= __popc(w);
-                        ++row;
-                        w = lds32a(cand_a + (row * 32 + col) * 4);
-                    }
-                    for (; skip; --skip) w ^= 1u << (31 - __clz(w));
-                }
-                // next candidate in (column, row) order: returns the window corner
-                auto pop = [&](uint32_t& dsta) -> uint32_t {
-                    while (w == 0) {
-                        if (++row == b1) {
-                            row = b0;
-                            ++col;
-                        }
-                        w = lds32a(cand_a + (row * 32 + col) * 4);
-                    }
-                    const uint32_t b = 31 - __clz(w);
-                    w ^= 1u << b;
-                    const uint32_t off = lbase(col) + static_cast<uint32_t>(row) * RP + bp_px(b);
-                    dsta = dst + off;
-                    return src + off - RP - 1;
-                };
-                const unsigned my = e > s ? e - s : 0u;
-                for (unsigned k = 0; k < my; k += 2) {
-                    uint32_t d0, d1 = 0;
-                    const uint32_t c0 = pop(d0);
-                    const bool two = k + 1 < my;
-                    uint32_t c1 = c0;
-                    if (two) c1 = pop(d1);
-                    const uint32_t v0 = bp_replace<ALE, RP>(c0, a.k7);
-                    const uint32_t v1 = bp_replace<ALE, RP>(c1, a.k7);
-                    sts8a(d0, v0);
-                    if (two) sts8a(d1, v1);
-                }
+            push(finalize(b0, of | oM, wf | wM | (of & oM)), b0);
+            if (pending) {
+                __syncwarp();
+                drain(0, pending);
             }
         }
         // per-tile counters of this iteration

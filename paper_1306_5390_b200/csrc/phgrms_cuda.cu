@@ -312,11 +312,11 @@ bool use_bp(const phg_params& p, int iters) {
     return !off && p.beta == 1 && p.border == PHG_BORDER_FAITHFUL && p.card_threshold <= 3 && iters <= 5;
 }
 
-// staged rows per tile (tunable: PHG_BP_ROWS); 48 keeps two CTAs per SM
+// staged rows per tile (tunable: PHG_BP_ROWS); 46 keeps two CTAs per SM
 int bp_rows_target() {
     static const int v = [] {
         const char* e = getenv("PHG_BP_ROWS");
-        return e ? std::max(8, std::min(phg::kBpMaxRows, atoi(e))) : 48;
+        return e ? std::max(8, std::min(phg::kBpMaxRows, atoi(e))) : phg::kBpMaxRows;
     }();
     return v;
 }
