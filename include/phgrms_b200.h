@@ -91,10 +91,13 @@ int phg_denoise_pass(const uint8_t* img, int width, int height, const int32_t* c
 
 /* denoise (denoise.hpp:292-311): iterate up to p->max_iterations, stop
  * after the first iteration that replaced nothing.  `stats` has capacity
- * p->max_iterations; *iterations_run entries are filled.  bands >= 2 runs
- * the row-band sharded engine (the reference's Parallel engine, row_blocks
- * partition, denoise.hpp:97-107) with halo exchange between bands on one
- * device; results are bit-identical for every band count. */
+ * p->max_iterations; *iterations_run entries are filled.  `bands` is the
+ * reference's Parallel engine worker count (row_blocks partition,
+ * denoise.hpp:97-107); results are bit-identical for every band count, so on
+ * one device any count runs the single-image pipeline.  With the environment
+ * variable PHG_BAND_ENGINE=1, bands >= 2 runs the row-band engine instead
+ * (halo exchange between bands on one device; a test hook for the band logic
+ * the multi-device paths share). */
 int phg_denoise(const uint8_t* img, int width, int height, const phg_params* p, int bands,
                 uint8_t* out, phg_pass_stats* stats, int* iterations_run);
 

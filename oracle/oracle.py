@@ -90,6 +90,10 @@ def ref():
                                   C.c_int, C.c_int, _u8p, _i64p, _i64p, C.POINTER(C.c_int)]
         R.ref_denoise_batch.argtypes = [_u8p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                         C.c_int, C.c_int, C.c_int, _u8p, _i32p]
+        R.ref_denoise_batch_stats.argtypes = [_u8p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                              C.c_int, C.c_int, C.c_int, _u8p, _i64p, _i64p, _i32p]
+        R.ref_denoise_band.argtypes = [_u8p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                       C.c_int, C.c_int, _u8p, _i64p, _i64p]
         R.ref_hardware_concurrency.restype = C.c_int
         _REF = R
     return _REF
@@ -228,6 +232,31 @@ def ref_denoise_batch(imgs, alpha=20, beta=1, k=5, thr=3, border=0, threads=1):
     its = np.zeros(n, np.int32)
     ref().ref_denoise_batch(imgs, n, w, h, alpha, beta, k, thr, border, threads, out, its)
     return out, its
+
+
+def ref_denoise_batch_stats(imgs, alpha=20, beta=1, k=5, thr=3, border=0, threads=1):
+    """The reference on a packed batch: (final images, per-image stats lists)."""
+    imgs = np.ascontiguousarray(imgs, np.uint8)
+    n, h, w = imgs.shape
+    out = np.empty_like(imgs)
+    fl = np.zeros((n, k), np.int64)
+    rp = np.zeros((n, k), np.int64)
+    its = np.zeros(n, np.int32)
+    assert ref().ref_denoise_batch_stats(imgs, n, w, h, alpha, beta, k, thr, border, threads, out, fl, rp,
+                                         its) == 0
+    return out, [[(int(fl[i, j]), int(rp[i, j])) for j in range(its[i])] for i in range(n)]
+
+
+def ref_denoise_band(band, own_lo, own_hi, alpha=20, beta=1, k=5, thr=3, border=0):
+    """k reference passes on a row band; (owned rows after k passes, owned
+    per-pass (flagged, replaced) over all k passes, untruncated)."""
+    band = np.ascontiguousarray(band, np.uint8)
+    bh, w = band.shape
+    out = np.empty((own_hi - own_lo, w), np.uint8)
+    fl = np.zeros(k, np.int64)
+    rp = np.zeros(k, np.int64)
+    assert ref().ref_denoise_band(band, w, bh, own_lo, own_hi, alpha, beta, k, thr, border, out, fl, rp) == 0
+    return out, [(int(fl[i]), int(rp[i])) for i in range(k)]
 
 
 # ---------------------------------------------------------------------------

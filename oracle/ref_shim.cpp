@@ -7,6 +7,7 @@
 // reference's own CPU path as bench.py's cpu_baseline ("kind": "reference").
 // Output: oracle/_ref/libphgrms_ref.so (git-ignored, travels with gpurun).
 // No reference source is copied into this repository.
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <stdexcept>
@@ -156,6 +157,66 @@ int ref_denoise_batch(const uint8_t* imgs, int n, int w, int h, int alpha, int b
     }
     for (auto& th : pool) th.join();
     return 0;
+}
+
+// Same as ref_denoise_batch, plus the per-iteration counters [n][k] (rows
+// past iterations_run[i] are left as they are).
+int ref_denoise_batch_stats(const uint8_t* imgs, int n, int w, int h, int alpha, int beta, int k, int thr,
+                            int border, int threads, uint8_t* out, int64_t* flagged, int64_t* replaced,
+                            int* iterations_run) {
+    const size_t px = static_cast<size_t>(w) * h;
+    const auto p = to_params(alpha, beta, k, thr, border);
+    auto work = [&](int lo, int hi) {
+        for (int i = lo; i < hi; ++i) {
+            const auto res = denoise(wrap(imgs + px * i, w, h), p, EngineSpec::serial());
+            std::memcpy(out + px * i, res.image.pixels.data(), px);
+            iterations_run[i] = static_cast<int>(res.stats.size());
+            for (size_t j = 0; j < res.stats.size(); ++j) {
+                flagged[static_cast<size_t>(i) * k + j] = res.stats[j].flagged;
+                replaced[static_cast<size_t>(i) * k + j] = res.stats[j].replaced;
+            }
+        }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 0; t < std::max(1, threads); ++t) {
+        const int lo = static_cast<int>(static_cast<int64_t>(n) * t / std::max(1, threads));
+        const int hi = static_cast<int>(static_cast<int64_t>(n) * (t + 1) / std::max(1, threads));
+        if (hi > lo) pool.emplace_back(work, lo, hi);
+    }
+    for (auto& th : pool) th.join();
+    return 0;
+}
+
+// One row band of a tall image, for golden digests of images too large to
+// denoise whole (C5, 2^32 px).  Band rows [0, bh) hold consecutive image
+// rows; the owned band rows [own_lo, own_hi) are at least beta*k rows from
+// every band edge that is not an image edge, so k passes of the reference
+// (compute_cardinality + detail::removal_rows, denoise.hpp:139-223) on the
+// band alone give their exact values: a fake edge corrupts one more row per
+// pass.  Runs all k passes (a zero-replacement pass is a fixed point, so
+// truncating after the global first zero is exact) and counts flagged /
+// replaced over the owned rows only.
+int ref_denoise_band(const uint8_t* band, int w, int bh, int own_lo, int own_hi, int alpha, int beta, int k,
+                     int thr, int border, uint8_t* out_owned, int64_t* flagged, int64_t* replaced) {
+    try {
+        const auto p = to_params(alpha, beta, k, thr, border);
+        GrayImage cur = wrap(band, w, bh);
+        for (int i = 0; i < k; ++i) {
+            const auto card = compute_cardinality(cur, alpha, beta, EngineSpec::serial());
+            GrayImage next = cur;
+            detail::removal_rows(cur, card, p, next.pixels.data(), 0, own_lo);
+            const auto c = detail::removal_rows(cur, card, p, next.pixels.data(), own_lo, own_hi);
+            detail::removal_rows(cur, card, p, next.pixels.data(), own_hi, bh);
+            flagged[i] = c.flagged;
+            replaced[i] = c.replaced;
+            cur = std::move(next);
+        }
+        std::memcpy(out_owned, cur.pixels.data() + static_cast<size_t>(own_lo) * w,
+                    static_cast<size_t>(own_hi - own_lo) * w);
+        return 0;
+    } catch (const std::invalid_argument&) {
+        return -1;
+    }
 }
 
 }  // extern "C"

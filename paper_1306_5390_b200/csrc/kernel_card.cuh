@@ -294,6 +294,7 @@ struct RemovalArgs {
     int alpha, thr, faithful;
     uint32_t k7;           // ((256-alpha) & 0x7f) in every byte
     unsigned long long* counters;  // [n][1][2]
+    int row0;              // first row of this launch's tile rows (grid.y <= 65535 per launch)
 };
 
 constexpr int kRmTW = 256;          // tile width (px)
@@ -322,7 +323,7 @@ __global__ void __launch_bounds__(256) removal_tile_kernel(const RemovalArgs a) 
     constexpr int W2 = (2 * BETA + 1) * (2 * BETA + 1);
     __shared__ __align__(16) uint8_t tile[(kRmTH + 2 * BETA) * kRmSP];
     const int img = blockIdx.z;
-    const int x0 = blockIdx.x * kRmTW, y0 = blockIdx.y * kRmTH;
+    const int x0 = blockIdx.x * kRmTW, y0 = a.row0 + blockIdx.y * kRmTH;
     const uint8_t* src = a.src + img * a.image_stride;
     // stage rows y0-BETA .. y0+kRmTH+BETA-1, columns x0-16 .. x0+kRmTW+16 (zeros outside)
     for (int i = threadIdx.x; i < (kRmTH + 2 * BETA) * (kRmSP / 16); i += 256) {

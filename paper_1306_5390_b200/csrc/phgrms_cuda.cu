@@ -77,6 +77,19 @@ int validate(const phg_params* p) {
     return PHG_OK;
 }
 
+// A band step's buffers must hold its owned rows plus the halo that lies
+// inside the image, and dst must have src's geometry (phg_dev_fused_step).
+int check_band(const phg_dev_image& src, const phg_dev_image& dst, int row_base, int height, int own_lo,
+               int own_hi, int halo) {
+    if (dst.width != src.width || dst.pitch != src.pitch || dst.n_images != src.n_images ||
+        dst.rows != src.rows || (src.n_images > 1 && dst.image_stride != src.image_stride))
+        return fail(PHG_EINVAL, "dst geometry differs from src");
+    const int need_lo = std::max(0, own_lo - halo), need_hi = std::min(height, own_hi + halo);
+    if (row_base > need_lo || static_cast<int64_t>(row_base) + src.rows < need_hi)
+        return fail(PHG_EINVAL, "band buffer does not hold the owned rows and their halo");
+    return PHG_OK;
+}
+
 int check_dims(int w, int h) {
     // GrayImage ctor (image.hpp:24-34)
     if (w < 1 || h < 1) return fail(PHG_EINVAL, "image dimensions must be >= 1");
@@ -471,10 +484,16 @@ int launch_card_tb(const phg_dev_image& src, int alpha, int beta, int32_t* card,
             PHG_TRY(encode_map(&m2, s2, sh));
             a2.card_out += static_cast<int64_t>(z0) * a.card_stride;
         }
-        dim3 grid(tiles_x, L.tiles_y, nz);
-        fn<<<grid, phg::kThreads, smem, stream>>>(m2, a2);
-        ++g_launches;
-        PHG_CUDA(cudaGetLastError());
+        // grid.y is capped at 65535: tall images run in pieces of tile rows,
+        // each starting its owned rows ty0 tiles further down
+        for (int ty0 = 0; ty0 < L.tiles_y; ty0 += 65535) {
+            phg::TileArgs a3 = a2;
+            a3.own_lo = a2.own_lo + ty0 * L.th;
+            dim3 grid(tiles_x, std::min(65535, L.tiles_y - ty0), nz);
+            fn<<<grid, phg::kThreads, smem, stream>>>(m2, a3);
+            ++g_launches;
+            PHG_CUDA(cudaGetLastError());
+        }
     }
     return PHG_OK;
 }
@@ -537,10 +556,14 @@ int launch_fused(const phg_dev_image& src, const phg_dev_image& dst, int row_bas
             a2.dst += z0 * dst.image_stride;
             a2.counters += static_cast<int64_t>(z0) * kcap * 2;
         }
-        dim3 grid(tiles_x, L.tiles_y, nz);
-        fn<<<grid, phg::kThreads, smem, stream>>>(m2, a2);
-        ++g_launches;
-        PHG_CUDA(cudaGetLastError());
+        for (int ty0 = 0; ty0 < L.tiles_y; ty0 += 65535) {
+            phg::TileArgs a3 = a2;
+            a3.own_lo = a2.own_lo + ty0 * L.th;
+            dim3 grid(tiles_x, std::min(65535, L.tiles_y - ty0), nz);
+            fn<<<grid, phg::kThreads, smem, stream>>>(m2, a3);
+            ++g_launches;
+            PHG_CUDA(cudaGetLastError());
+        }
     }
     return PHG_OK;
 }
@@ -949,6 +972,7 @@ int phg_dev_fused_step(const phg_dev_image* src, const phg_dev_image* dst, int r
     if (!src || !dst || own_lo < 0 || own_hi > height || own_lo >= own_hi || iters < 1 ||
         it0 < 0 || it0 + iters > kcap)
         return fail(PHG_EINVAL, "bad band geometry");
+    PHG_TRY(check_band(*src, *dst, row_base, height, own_lo, own_hi, p->beta * iters));
     if (max_fused(p->beta) > 0 && iters > max_fused(p->beta))
         return fail(PHG_EINVAL, "iters exceeds phg_max_fused_iterations(beta)");
     return step(*src, *dst, row_base, height, own_lo, own_hi, *p, it0, iters, counters, kcap,
@@ -963,6 +987,7 @@ int phg_dev_fused_step_mirrored(const phg_dev_image* src, const phg_dev_image* d
     if (!src || !dst || own_lo < 0 || own_hi > height || own_lo >= own_hi || iters < 1 || it0 < 0 ||
         it0 + iters > kcap)
         return fail(PHG_EINVAL, "bad band geometry");
+    PHG_TRY(check_band(*src, *dst, row_base, height, own_lo, own_hi, p->beta * iters));
     if (max_fused(p->beta) > 0 && iters > max_fused(p->beta))
         return fail(PHG_EINVAL, "iters exceeds phg_max_fused_iterations(beta)");
     if (npeers < 0 || npeers > 2 || (npeers > 0 && !peers)) return fail(PHG_EINVAL, "at most two halo peers");
@@ -1135,21 +1160,26 @@ int phg_dev_removal(const phg_dev_image* src, const int32_t* card, int64_t card_
             a2.dst += z0 * src->image_stride;
             a2.card += z0 * a.card_stride;
             if (a2.counters) a2.counters += static_cast<int64_t>(z0) * 2;
-            dim3 grid((src->width + phg::kRmTW - 1) / phg::kRmTW, (src->rows + phg::kRmTH - 1) / phg::kRmTH,
-                      std::min(65535, src->n_images - z0));
-            if (p->beta == 1) {
-                if (ale && vec) phg::removal_tile_kernel<true, true, 1><<<grid, 256, 0, st>>>(a2);
-                else if (ale) phg::removal_tile_kernel<true, false, 1><<<grid, 256, 0, st>>>(a2);
-                else if (vec) phg::removal_tile_kernel<false, true, 1><<<grid, 256, 0, st>>>(a2);
-                else phg::removal_tile_kernel<false, false, 1><<<grid, 256, 0, st>>>(a2);
-            } else {
-                if (ale && vec) phg::removal_tile_kernel<true, true, 2><<<grid, 256, 0, st>>>(a2);
-                else if (ale) phg::removal_tile_kernel<true, false, 2><<<grid, 256, 0, st>>>(a2);
-                else if (vec) phg::removal_tile_kernel<false, true, 2><<<grid, 256, 0, st>>>(a2);
-                else phg::removal_tile_kernel<false, false, 2><<<grid, 256, 0, st>>>(a2);
+            // grid.y is capped at 65535: tall images run in pieces of tile rows
+            const int tiles_y = (src->rows + phg::kRmTH - 1) / phg::kRmTH;
+            for (int ty0 = 0; ty0 < tiles_y; ty0 += 65535) {
+                a2.row0 = ty0 * phg::kRmTH;
+                dim3 grid((src->width + phg::kRmTW - 1) / phg::kRmTW, std::min(65535, tiles_y - ty0),
+                          std::min(65535, src->n_images - z0));
+                if (p->beta == 1) {
+                    if (ale && vec) phg::removal_tile_kernel<true, true, 1><<<grid, 256, 0, st>>>(a2);
+                    else if (ale) phg::removal_tile_kernel<true, false, 1><<<grid, 256, 0, st>>>(a2);
+                    else if (vec) phg::removal_tile_kernel<false, true, 1><<<grid, 256, 0, st>>>(a2);
+                    else phg::removal_tile_kernel<false, false, 1><<<grid, 256, 0, st>>>(a2);
+                } else {
+                    if (ale && vec) phg::removal_tile_kernel<true, true, 2><<<grid, 256, 0, st>>>(a2);
+                    else if (ale) phg::removal_tile_kernel<true, false, 2><<<grid, 256, 0, st>>>(a2);
+                    else if (vec) phg::removal_tile_kernel<false, true, 2><<<grid, 256, 0, st>>>(a2);
+                    else phg::removal_tile_kernel<false, false, 2><<<grid, 256, 0, st>>>(a2);
+                }
+                ++g_launches;
+                PHG_CUDA(cudaGetLastError());
             }
-            ++g_launches;
-            PHG_CUDA(cudaGetLastError());
         }
         return PHG_OK;
     }
@@ -1429,7 +1459,11 @@ int denoise_rows_pipelined(DeviceState* s, const uint8_t* img, int w, int h, con
 // (<= 8), never shorter than 32 rows.  PHG_ROW_CHUNKS / PHG_ROW_PIECES
 // override.  Rows already 16-byte pitched (width % 16 == 0) are copied
 // straight into / out of the pitched buffers.
-void row_plan_for(int w, int h, int& nchunks, int& npieces) {
+// `halo` = beta * (iterations of the deepest launch): every chunk must be at
+// least that tall, or a launch would read rows two chunks away that the
+// wavefront has not produced yet (and its ping-pong overwrite would race
+// with their readers).
+void row_plan_for(int w, int h, int halo, int& nchunks, int& npieces) {
     const char* ev = getenv("PHG_ROW_CHUNKS");  // read per call (tuning sweeps)
     const int env = ev ? std::max(0, std::min(8, atoi(ev))) : -1;
     const char* pv = getenv("PHG_ROW_PIECES");
@@ -1440,14 +1474,22 @@ void row_plan_for(int w, int h, int& nchunks, int& npieces) {
     if (env < 0 && bytes < (int64_t(32) << 20)) {  // 4K-class images: 3 chunks, 8 pieces (C2: 98 -> 118 K)
         nchunks = std::max(1, std::min(3, h / 32));
         npieces = std::max(nchunks, std::min(8, h / 32));
-        return;
+    } else {
+        nchunks = env > 0 ? env : static_cast<int>(std::min<int64_t>(8, bytes >> 23));
+        nchunks = std::max(1, std::min(nchunks, h / 32));
+        npieces = static_cast<int>(std::max<int64_t>(nchunks, std::min<int64_t>(kMaxRowChunks, bytes >> 21)));
+        if (pv) npieces = std::max(1, std::min(kMaxRowChunks, atoi(pv)));
+        npieces = std::min(npieces, h / 32);
+        npieces = std::max(npieces, nchunks);
     }
-    nchunks = env > 0 ? env : static_cast<int>(std::min<int64_t>(8, bytes >> 23));
-    nchunks = std::max(1, std::min(nchunks, h / 32));
-    npieces = static_cast<int>(std::max<int64_t>(nchunks, std::min<int64_t>(kMaxRowChunks, bytes >> 21)));
-    if (pv) npieces = std::max(1, std::min(kMaxRowChunks, atoi(pv)));
-    npieces = std::min(npieces, h / 32);
+    const int min_rows = std::max(32, halo);
+    if (nchunks > 1 && h / nchunks < min_rows) nchunks = std::max(1, h / min_rows);
     npieces = std::max(npieces, nchunks);
+}
+
+int pipeline_halo(const phg_params& p) {
+    const std::vector<int> plan = chunk_plan(p.max_iterations, p.beta);
+    return p.beta * (max_fused(p.beta) > 0 ? *std::max_element(plan.begin(), plan.end()) : 1);
 }
 
 int phg_denoise(const uint8_t* img, int w, int h, const phg_params* p, int bands, uint8_t* out,
@@ -1465,8 +1507,14 @@ int phg_denoise(const uint8_t* img, int w, int h, const phg_params* p, int bands
     PHG_TRY(scratch(s, 4, sizeof(uint64_t) * 2 * k, &pk));
     phg_dev_image im = make_image(pi, w, h, 1), am = make_image(pa, w, h, 1), bm = make_image(pb, w, h, 1);
     uint64_t* ctr = static_cast<uint64_t*>(pk);
+    // EngineSpec::parallel(W) on one device: the result does not depend on
+    // the partition (denoise.hpp:97-135), so W row bands would only add
+    // launches and halo copies -- the single-image pipeline runs instead.
+    // PHG_BAND_ENGINE=1 keeps the W-band engine (test hook for the band and
+    // halo logic that the multi-device paths share).
+    if (bands > 1 && !getenv("PHG_BAND_ENGINE")) bands = 1;
     int rchunks = 0, rpieces = 0;
-    if (bands <= 1) row_plan_for(w, h, rchunks, rpieces);
+    if (bands <= 1) row_plan_for(w, h, pipeline_halo(*p), rchunks, rpieces);
     if (rchunks > 0) {
         PHG_TRY(denoise_rows_pipelined(s, img, w, h, *p, out, ctr, rchunks, rpieces));
         std::vector<uint64_t> hc(2 * k);
@@ -1501,7 +1549,7 @@ int phg_denoise_batch(const uint8_t* imgs, int n, int w, int h, const phg_params
     if (n < 1) return fail(PHG_EINVAL, "batch must hold at least one image");
     if (n == 1) {
         int rc = 0, rp = 0;
-        row_plan_for(w, h, rc, rp);
+        row_plan_for(w, h, pipeline_halo(*p), rc, rp);
         if (rc > 0) return phg_denoise(imgs, w, h, p, 1, out, stats, iterations_run);
     }
     DeviceState* s;

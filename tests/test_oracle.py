@@ -174,3 +174,22 @@ def test_band_pass_equals_full_image():
             out[lo:hi] = bout[lo - blo:hi - blo]
             tf, tr = tf + ff, tr + rr
         assert np.array_equal(out, full) and (tf, tr) == (f, r)
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+def test_band_wise_reference_equals_whole_image():
+    """Pins the method behind the C5 golden digest (tests/golden/make_golden.py
+    c5_full): k reference passes on row bands with a beta*k-row halo give the
+    whole-image reference's image, and the owned-row counters sum to its
+    per-iteration stats."""
+    img = O.ref_inject_sp_noise(O.ref_synth_image(700, 333, 4), 0.3, 0.5, 8)
+    fin, st = O.ref_denoise(img)
+    parts, tot = [], np.zeros((5, 2), np.int64)
+    for lo in range(0, 333, 50):
+        hi = min(333, lo + 50)
+        blo, bhi = max(0, lo - 5), min(333, hi + 5)
+        out, bst = O.ref_denoise_band(img[blo:bhi], lo - blo, hi - blo)
+        parts.append(out)
+        tot += np.array(bst, np.int64)
+    assert np.array_equal(np.concatenate(parts), fin)
+    assert [tuple(int(x) for x in r) for r in tot[:len(st)]] == st

@@ -171,8 +171,13 @@ def test_ragged_shapes(w, h, beta):
 
 
 # ------------------------------------------------------- partition invariance
+@pytest.mark.parametrize("band_engine", [False, True])
 @pytest.mark.parametrize("bands", [2, 3, 8])
-def test_parallel_bands_equal_serial(bands):
+def test_parallel_bands_equal_serial(bands, band_engine, monkeypatch):
+    # default: Parallel(W) runs the single-image pipeline; PHG_BAND_ENGINE=1
+    # runs W row bands with halo exchange on the device
+    if band_engine:
+        monkeypatch.setenv("PHG_BAND_ENGINE", "1")
     rng = np.random.default_rng(201)
     for _ in range(25):
         w, h = int(rng.integers(1, 33)), int(rng.integers(1, 33))
@@ -181,8 +186,11 @@ def test_parallel_bands_equal_serial(bands):
         _check_denoise(img, alpha, beta, 5, 3, border, bands=bands)
 
 
+@pytest.mark.parametrize("band_engine", [False, True])
 @pytest.mark.parametrize("bands", [2, 5, 16])
-def test_parallel_bands_large(bands):
+def test_parallel_bands_large(bands, band_engine, monkeypatch):
+    if band_engine:
+        monkeypatch.setenv("PHG_BAND_ENGINE", "1")
     clean = O.synth_image(700, 555, 5)
     noisy = O.inject_sp_noise(clean, 0.3, 0.5, 5)
     for beta in (1, 2):
