@@ -184,6 +184,7 @@ def c5_full(size=65536, band=1024, k=5):
         return tiles[ti]
 
     h_in, h_out = hashlib.sha256(), hashlib.sha256()
+    blocks = []  # short digests of each band's final rows (multi-rank parity checks)
     per_it = np.zeros((k, 2), np.int64)
     bands = [(lo, min(size, lo + band)) for lo in range(0, size, band)]
 
@@ -206,6 +207,7 @@ def c5_full(size=65536, band=1024, k=5):
             for noisy_rows, out, st in ex.map(run, mine):
                 h_in.update(noisy_rows.tobytes())
                 h_out.update(out.tobytes())
+                blocks.append(hashlib.sha256(out.tobytes()).hexdigest()[:16])
                 per_it += np.array(st, np.int64)
             for tt in list(tiles):
                 if tt < ti:
@@ -217,14 +219,14 @@ def c5_full(size=65536, band=1024, k=5):
         if per_it[j, 1] == 0:
             break  # denoise.hpp:308 (later passes were fixed points)
     return dict(w=size, h=size, density=0.30, beta=1, k=k, tile=tile, noisy=h_in.hexdigest(),
-                final=h_out.hexdigest(), stats=stats)
+                final=h_out.hexdigest(), stats=stats, block_rows=band, final_blocks=blocks)
 
 
 def full_configs():
     path = os.path.join(HERE, "digests_full.json")
     out = json.load(open(path)) if os.path.exists(path) else {}
     for name, fn in (("c4", c4_full), ("c3", c3_full), ("c5", c5_full)):
-        if name in out and "--force" not in sys.argv:
+        if name in out and "--force" not in sys.argv and f"--redo-{name}" not in sys.argv:
             continue
         print("computing", name, flush=True)
         out[name] = fn()
