@@ -396,16 +396,19 @@ __global__ void __launch_bounds__(kBpThreads, 2)
                 rv = rvn;
             }
             // credits of the pairs (b1-1, b1) for the next band's first row
+            // (handed over through named barrier 1 + warp: this warp arrives,
+            // the warp below waits -- no CTA-wide barrier in mid-iteration)
             if (warp + 1 < nb) {
                 const uint32_t sse = bp_shE(seP, west);
                 const uint32_t dn = down_a + (warp * 32 + lane) * 8;
                 sts32a(dn, oP | sse);
                 sts32a(dn + 4, wP | (oP & sse));  // maj3(s, sw, sse)
+                asm volatile("bar.arrive %0, 64;" ::"r"(1 + warp) : "memory");
             }
         }
-        __syncthreads();  // the band edges are in place; dst rows of every band copied
         if (active) {
             if (warp > 0) {
+                asm volatile("bar.sync %0, 64;" ::"r"(warp) : "memory");
                 const uint32_t dn = down_a + ((warp - 1) * 32 + lane) * 8;
                 oM = lds32a(dn);
                 wM = lds32a(dn + 4);
