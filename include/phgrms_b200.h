@@ -101,6 +101,16 @@ int phg_denoise_pass(const uint8_t* img, int width, int height, const int32_t* c
 int phg_denoise(const uint8_t* img, int width, int height, const phg_params* p, int bands,
                 uint8_t* out, phg_pass_stats* stats, int* iterations_run);
 
+/* Denoise of a binary PGM file (P5, maxval <= 255) into a P5 file, with the
+ * file I/O overlapped with the host<->device copies: the raster is read in
+ * ~16 MB row chunks into pinned staging buffers while earlier chunks are
+ * copied to the device, and the result is written while later chunks come
+ * back.  Header parsing, error texts and the written
+ * file are the reference's read_pgm / write_pgm (pgm.hpp:98-150); P2 input
+ * returns PHG_EINVAL (the drop-in falls back to load_pgm). */
+int phg_denoise_pgm_file(const char* in_path, const char* out_path, const phg_params* p,
+                         phg_pass_stats* stats, int* iterations_run);
+
 /* Batch of n independent images packed [n][height][width]; stats is
  * [n][max_iterations], iterations_run is [n]. */
 int phg_denoise_batch(const uint8_t* imgs, int n, int width, int height, const phg_params* p,

@@ -23,6 +23,7 @@ from .phgrms import (  # noqa: F401
     denoise_batch,
     denoise_sharded,
     denoise_pass,
+    denoise_pgm_file,
     inject_sp_noise,
     format_db,
     kernel_name,

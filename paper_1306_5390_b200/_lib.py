@@ -25,7 +25,7 @@ EXPORTS = (
     "phg_dev_denoise", "phg_dev_cardinality", "phg_dev_removal", "phg_finalize_stats",
     "phg_fused_kernel_name", "phg_residual_noise_count", "phg_sse", "phg_dev_residual_count", "phg_dev_sse",
     "phg_dev_synth_smooth", "phg_dev_inject_noise", "phg_denoise_sharded", "phg_dev_fused_step_mirrored",
-    "phg_ipc_get_handle", "phg_ipc_open_handle", "phg_ipc_close", "phg_debug_rms",
+    "phg_ipc_get_handle", "phg_ipc_open_handle", "phg_ipc_close", "phg_debug_rms", "phg_denoise_pgm_file",
 )
 
 
@@ -118,6 +118,8 @@ def lib():
         L.phg_residual_noise_count.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                                C.POINTER(C.c_uint64)]
         L.phg_debug_rms.argtypes = [C.c_int, C.c_uint32, C.c_void_p]
+        L.phg_denoise_pgm_file.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(PhgParams), C.c_void_p,
+                                           C.POINTER(C.c_int)]
         L.phg_sse.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_uint64)]
         L.phg_dev_residual_count.argtypes = [C.POINTER(PhgDevImage), C.c_int, C.c_int, C.c_int, C.c_void_p,
                                              C.c_void_p]

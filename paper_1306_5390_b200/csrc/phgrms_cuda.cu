@@ -31,6 +31,15 @@
 #include "kernel_h2b2.cuh"
 #include "kernels.cuh"
 
+namespace {
+thread_local std::string g_error;
+}
+
+// phg_last_error() for the entry points of the other translation units (pgm_io.cu)
+namespace phg_internal {
+void set_error(const std::string& msg) { g_error = msg; }
+}  // namespace phg_internal
+
 // phg_debug_rms: the fused kernels' RMS replacement for every S < n.
 __global__ void rms_probe_kernel(uint32_t f, float rcp_f, uint32_t n, uint32_t* out) {
     const uint32_t S = blockIdx.x * blockDim.x + threadIdx.x;
@@ -39,7 +48,6 @@ __global__ void rms_probe_kernel(uint32_t f, float rcp_f, uint32_t n, uint32_t* 
 
 namespace {
 
-thread_local std::string g_error;
 thread_local int64_t g_launches = 0;
 
 int fail(int code, const std::string& msg) {

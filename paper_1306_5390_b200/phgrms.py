@@ -383,6 +383,22 @@ def cardmap(img: GrayImage, alpha: int = 20, beta: int = 1) -> str:
     return write_p2(card.width, card.height, card.counts, (2 * beta + 1) * (2 * beta + 1))
 
 
+def denoise_pgm_file(in_path: str, out_path: str, params: DenoiseParams = None) -> List[PassStats]:
+    """Denoise a binary PGM file into a P5 file with the file reads and writes
+    overlapped with the host<->device copies (phg_denoise_pgm_file, SURVEY.md
+    8(f) f4); the written file is the reference's write_pgm of the result
+    (pgm.hpp:142-150).  Returns the per-iteration stats."""
+    params = params or DenoiseParams()
+    params.validate()
+    k = params.max_iterations
+    stats = (PhgPassStats * k)()
+    it = C.c_int()
+    p = params._c()
+    check(lib().phg_denoise_pgm_file(os.fsencode(in_path), os.fsencode(out_path), C.byref(p), stats,
+                                     C.byref(it)))
+    return [PassStats(s.iteration, s.flagged, s.replaced, s.elapsed_ms) for s in stats[: it.value]]
+
+
 def kernel_name(params: DenoiseParams, iters: int) -> str:
     """Which sm_100a kernel a fused launch of `iters` iterations runs for
     these parameters (phg_fused_kernel_name)."""

@@ -3,6 +3,7 @@
 // drop-in headers in include/phgrms/ -- i.e. code written for the reference
 // API, unchanged, now running on the B200 kernels.  Built by
 // __graft_entry__.build(); run by tests/test_dropin_gpu.py on a GPU.
+#include <cmath>
 #include <cstdio>
 #include <fstream>
 #include <iterator>
@@ -13,6 +14,7 @@
 #include <stdexcept>
 
 #include "phgrms/bench.hpp"
+#include "phgrms/pgm_gpu.hpp"
 #include "phgrms/denoise.hpp"
 #include "phgrms/image.hpp"
 #include "phgrms/metrics.hpp"
@@ -337,6 +339,33 @@ int main(int argc, char** argv) {
         std::ifstream gf(g_golden_dir + "/bench_grid.csv");
         const std::string want((std::istreambuf_iterator<char>(gf)), std::istreambuf_iterator<char>());
         CHECK(!want.empty() && got == want);
+        // GPU columns (opt-in CSV): device time, rate and roofline fraction
+        const std::string gcsv = write_csv_gpu(r5.records);
+        CHECK(gcsv.rfind(hdr.substr(0, hdr.size() - 1) + ",device_ms,mpix_it_per_s,hbm_roofline_frac\n", 0) == 0);
+        for (const auto& r : r5.records)
+            CHECK(r.device_ms > 0.0 && r.mpix_it_per_s > 0.0 && r.hbm_roofline_frac > 0.0 &&
+                  std::abs(r.mpix_it_per_s - double(r.width) * r.height * r.iterations_run / (r.device_ms * 1e3)) <
+                      1e-6 * r.mpix_it_per_s);
+    }
+    {  // pgm_gpu.hpp: file -> device -> file equals save_pgm(denoise(load_pgm))
+        const auto clean = synth_image(700, 300, 3, SynthKind::SmoothRandom);
+        NoiseSpec spec;
+        spec.density = 0.3;
+        spec.seed = 9;
+        const auto noisy = inject_sp_noise(clean, spec).first;
+        for (const bool ascii : {false, true}) {
+            const std::string in = std::string("/tmp/phg_dropin_in") + (ascii ? "2" : "5") + ".pgm";
+            const std::string out = "/tmp/phg_dropin_out.pgm", want = "/tmp/phg_dropin_want.pgm";
+            save_pgm(in, noisy, ascii);
+            const auto st = denoise_pgm_file(in, out);
+            const auto ref = denoise(noisy, DenoiseParams{});
+            save_pgm(want, ref.image);
+            std::ifstream a(out, std::ios::binary), b(want, std::ios::binary);
+            const std::string ga((std::istreambuf_iterator<char>(a)), std::istreambuf_iterator<char>());
+            const std::string gb((std::istreambuf_iterator<char>(b)), std::istreambuf_iterator<char>());
+            CHECK(!ga.empty() && ga == gb && st.size() == ref.stats.size());
+        }
+        CHECK_THROWS_AS(denoise_pgm_file("/nonexistent/x.pgm", "/tmp/phg_x.pgm"), PgmError);
     }
     std::printf("dropin: %d checks, %d failures\n", g_checks, g_fail);
     return g_fail ? 1 : 0;
