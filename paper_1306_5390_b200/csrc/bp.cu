@@ -5,6 +5,7 @@
 
 #include "bp_launch.h"
 #include "kernel_bp.cuh"
+#include "kernel_bp2.cuh"
 
 namespace phg {
 
@@ -29,7 +30,38 @@ BpFn select(int T, bool ale, bool wide) {
     }
 }
 
+template <int T>
+BpFn pick2(bool ale, bool wide) {
+    if (wide) return ale ? fused_bp2_kernel<T, true, true> : fused_bp2_kernel<T, false, true>;
+    return ale ? fused_bp2_kernel<T, true, false> : fused_bp2_kernel<T, false, false>;
+}
+
+BpFn select2(int T, bool ale, bool wide) {
+    switch (T) {
+        case 1: return pick2<1>(ale, wide);
+        case 2: return pick2<2>(ale, wide);
+        case 3: return pick2<3>(ale, wide);
+        case 4: return pick2<4>(ale, wide);
+        default: return nullptr;
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_bp2_kernel(int T, bool ale, bool wide, const CUtensorMap& map, const BpArgs& a, unsigned grid,
+                              size_t smem, cudaStream_t stream) {
+    BpFn fn = select2(T, ale, wide);
+    if (!fn) return cudaErrorInvalidValue;
+    if (smem > bp2_smem(kBp2MaxRows)) return cudaErrorInvalidValue;
+    cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(bp2_smem(kBp2MaxRows)));
+    if (e != cudaSuccess) return e;
+    fn<<<grid, kBpThreads, smem, stream>>>(map, a);
+    return cudaGetLastError();
+}
+
+size_t bp2_smem(int sh) { return static_cast<size_t>(bp2_smem_bytes(sh)); }
 
 cudaError_t launch_bp_kernel(int T, bool ale, bool wide, const CUtensorMap& map, const BpArgs& a, unsigned grid,
                              size_t smem, cudaStream_t stream) {

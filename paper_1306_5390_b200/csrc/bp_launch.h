@@ -10,7 +10,8 @@
 
 namespace phg {
 
-constexpr int kBpMaxRows = 46;  // staged rows: two CTAs per SM
+constexpr int kBpMaxRows = 46;   // staged rows: two CTAs per SM (beta = 1)
+constexpr int kBp2MaxRows = 45;  // beta = 2 (larger band-edge handover)
 
 struct BpArgs {
     uint8_t* dst;
@@ -43,5 +44,9 @@ cudaError_t launch_bp_kernel(int T, bool ale, bool wide, const CUtensorMap& map,
                              size_t smem, cudaStream_t stream);
 // dynamic shared memory of one CTA staging sh rows
 size_t bp_smem(int sh);
+// the beta = 2 kernel (kernel_bp2.cuh), T <= 4
+cudaError_t launch_bp2_kernel(int T, bool ale, bool wide, const CUtensorMap& map, const BpArgs& a, unsigned grid,
+                              size_t smem, cudaStream_t stream);
+size_t bp2_smem(int sh);
 
 }  // namespace phg

@@ -355,16 +355,25 @@ BpCols bp_cols(int width) {
     return {true, (width + 991) / 992, 992, 16};
 }
 
+// beta = 2, Faithful, card_threshold <= 3: the packed-bit beta = 2 kernel
+// (kernel_bp2.cuh; PHG_NO_BP2=1 falls back to fused_h2b2_kernel)
+bool use_bp2(const phg_params& p, int iters) {
+    static const bool off = getenv("PHG_NO_BP2") != nullptr;
+    return !off && p.beta == 2 && p.border == PHG_BORDER_FAITHFUL && p.card_threshold <= 3 && iters <= 4;
+}
+
 int launch_bp(const phg_dev_image& src, const phg_dev_image& dst, int row_base, int height, int own_lo,
               int own_hi, const phg_params& p, int it0, int iters, uint64_t* counters, int kcap,
               cudaStream_t stream, const phg::HaloPeers& peers, bool early) {
-    const int halo = iters;
+    const bool b2 = p.beta == 2;
+    const int halo = p.beta * iters;
+    const int max_rows = b2 ? phg::kBp2MaxRows : phg::kBpMaxRows;
     const BpCols cols = bp_cols(src.width);
-    const Launch L = plan_rows_h2(own_hi - own_lo, halo, bp_rows_target(), src.n_images, cols.tiles_x,
-                                  cols.wide ? 1 : 2);
+    const Launch L = plan_rows_h2(own_hi - own_lo, halo, std::min(bp_rows_target(), max_rows), src.n_images,
+                                  cols.tiles_x, cols.wide ? 1 : 2);
     const int sh = L.th + 2 * halo;
-    if (sh > phg::kBpMaxRows) return fail(PHG_EINVAL, "tile too tall");
-    const size_t smem = phg::bp_smem(sh);
+    if (sh > max_rows) return fail(PHG_EINVAL, "tile too tall");
+    const size_t smem = b2 ? phg::bp2_smem(sh) : phg::bp_smem(sh);
     CUtensorMap map;
     PHG_TRY(encode_map(&map, src, sh, cols.wide ? 64 : 32));
     phg::BpArgs a{};
@@ -394,7 +403,10 @@ int launch_bp(const phg_dev_image& src, const phg_dev_image& dst, int row_base, 
     a.counters = reinterpret_cast<unsigned long long*>(counters);
     a.peers = peers;
     const unsigned grid = static_cast<unsigned>(cols.wide ? n_tiles : (n_tiles + 1) / 2);
-    PHG_CUDA(phg::launch_bp_kernel(iters, p.alpha <= 128, cols.wide, map, a, grid, smem, stream));
+    if (b2)
+        PHG_CUDA(phg::launch_bp2_kernel(iters, p.alpha <= 128, cols.wide, map, a, grid, smem, stream));
+    else
+        PHG_CUDA(phg::launch_bp_kernel(iters, p.alpha <= 128, cols.wide, map, a, grid, smem, stream));
     ++g_launches;
     return PHG_OK;
 }
@@ -510,7 +522,7 @@ int launch_fused(const phg_dev_image& src, const phg_dev_image& dst, int row_bas
                  int own_lo, int own_hi, const phg_params& p, int it0, int iters,
                  uint64_t* counters, int kcap, cudaStream_t stream, const phg::HaloPeers& peers = kNoPeers,
                  bool early = false) {
-    if (use_bp(p, iters))
+    if (use_bp(p, iters) || use_bp2(p, iters))
         return launch_bp(src, dst, row_base, height, own_lo, own_hi, p, it0, iters, counters, kcap, stream, peers,
                          early);
     if (use_h2(p, iters))
@@ -948,7 +960,10 @@ const char* phg_fused_kernel_name(const phg_params* p, int iters) {
                                        "fused_h2b2_kernel<T=3>", "fused_h2b2_kernel<T=4>"};
     static const char* const bp[] = {"", "fused_bp_kernel<T=1>", "fused_bp_kernel<T=2>", "fused_bp_kernel<T=3>",
                                      "fused_bp_kernel<T=4>", "fused_bp_kernel<T=5>"};
+    static const char* const bp2[] = {"", "fused_bp2_kernel<T=1>", "fused_bp2_kernel<T=2>",
+                                      "fused_bp2_kernel<T=3>", "fused_bp2_kernel<T=4>"};
     if (use_bp(*p, iters)) return bp[iters];
+    if (use_bp2(*p, iters)) return bp2[iters];
     if (use_h2(*p, iters)) return h2[iters];
     if (use_h2b2(*p, iters)) return h2b2[iters];
     return p->beta == 1 ? b1[iters] : p->beta == 2 ? b2[iters] : b3[iters];

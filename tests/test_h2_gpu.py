@@ -30,7 +30,7 @@ def test_kernel_selected():
     L = P.lib()
     assert P.kernel_name(P.DenoiseParams(), 5) == "fused_bp_kernel<T=5>"
     assert P.kernel_name(P.DenoiseParams(card_threshold=4), 5).startswith("fused_tb_kernel")
-    assert P.kernel_name(P.DenoiseParams(beta=2), 4) == "fused_h2b2_kernel<T=4>"
+    assert P.kernel_name(P.DenoiseParams(beta=2), 4) == "fused_bp2_kernel<T=4>"
     assert P.kernel_name(P.DenoiseParams(beta=2, border=P.BorderMode(1)), 4).startswith("fused_tb_kernel")
     assert P.kernel_name(P.DenoiseParams(beta=2, card_threshold=4), 4).startswith("fused_tb_kernel")
     assert L is not None

@@ -28,8 +28,8 @@ def _check(noisy, alpha=20, k=5, thr=3):
 
 
 def test_kernel_selected():
-    assert P.kernel_name(P.DenoiseParams(beta=2), 4) == "fused_h2b2_kernel<T=4>"
-    assert P.kernel_name(P.DenoiseParams(beta=2, card_threshold=3), 2) == "fused_h2b2_kernel<T=2>"
+    assert P.kernel_name(P.DenoiseParams(beta=2), 4) == "fused_bp2_kernel<T=4>"
+    assert P.kernel_name(P.DenoiseParams(beta=2, card_threshold=3), 2) == "fused_bp2_kernel<T=2>"
     assert P.kernel_name(P.DenoiseParams(beta=2, card_threshold=4), 4).startswith("fused_tb_kernel")
 
 
