@@ -396,21 +396,21 @@ __global__ void __launch_bounds__(kBpThreads, 2)
         constexpr int kChunksRow = RP / 16;
         const int c_lo = a.x_apron / 16;
         const int c_n = WIDE ? a.x_step / 16 : kChunksRow;
-        const int rows = max(outA, outB);
-        for (int i = tid; i < NH * rows * c_n; i += kBpThreads) {
-            const int hh = WIDE ? 0 : i / (rows * c_n);
-            const int rem = i - hh * rows * c_n;
-            const int r = rem / c_n, ch = c_lo + rem - r * c_n;
+        // warps over (tile, row), lanes over the row's 16-byte chunks
+        for (int hh = 0; hh < NH; ++hh) {
             const int out_h = hh ? outB : outA;
             const int x0h = hh ? x0B : x0A;
-            if (r >= out_h || x0h + 16 * ch >= a.width) continue;
-            const int y = HALO + r;
-            const uint4 v = *reinterpret_cast<const uint4*>(fin + hh * half_bytes + y * RP + 16 * ch);
-            const int imgh = hh ? imgB : imgA;
+            uint8_t* gdst = a.dst + (hh ? imgB : imgA) * a.image_stride;
             const int y0h = hh ? y0B : y0A;
-            *reinterpret_cast<uint4*>(a.dst + imgh * a.image_stride + static_cast<int64_t>(y0h + y) * a.pitch +
-                                      x0h + 16 * ch) = v;
-            mirror_row16(a.peers, a.row_base + y0h + y, a.pitch, x0h + 16 * ch, v);
+            for (int r = warp; r < out_h; r += kBpWarps) {
+                const int y = HALO + r;
+                for (int ch = c_lo + lane; ch < c_lo + c_n; ch += 32) {
+                    if (x0h + 16 * ch >= a.width) break;
+                    const uint4 v = *reinterpret_cast<const uint4*>(fin + hh * half_bytes + y * RP + 16 * ch);
+                    *reinterpret_cast<uint4*>(gdst + static_cast<int64_t>(y0h + y) * a.pitch + x0h + 16 * ch) = v;
+                    mirror_row16(a.peers, a.row_base + y0h + y, a.pitch, x0h + 16 * ch, v);
+                }
+            }
         }
     }
     if (tid < 4 * T && nit > 0) {
