@@ -434,7 +434,17 @@ __global__ void __launch_bounds__(kBpThreads, 2)
             if (rpA) atomicAdd(&red[t][2], rpA);
             if (rpB) atomicAdd(&red[t][3], rpB);
         }
-        __syncthreads();
+        // End of iteration t.  Iteration t+1 reads, around its band, rows at
+        // most 3 above and 2 below it -- rows of this warp's two neighbours
+        // when every band of both iterations holds >= 3 rows.  Then only the
+        // neighbours are waited for (pairwise named barriers 8 + w for warps
+        // w, w+1); otherwise, and before the output stores, the whole CTA.
+        if (t + 1 < nit && n - 2 >= 3 * kBpWarps) {
+            if (warp > 0) asm volatile("bar.sync %0, 64;" ::"r"(8 + warp - 1) : "memory");
+            if (warp + 1 < kBpWarps) asm volatile("bar.sync %0, 64;" ::"r"(8 + warp) : "memory");
+        } else {
+            __syncthreads();
+        }
     }
 
     // ---- owned output rows: 16-byte coalesced stores
