@@ -58,7 +58,12 @@ namespace phg {
 constexpr int kBpWarps = 8;
 constexpr int kBpThreads = 32 * kBpWarps;
 constexpr int kBpPad = 128;        // dynamic smem starts with a pad (window reads at region column -1)
-constexpr int kBpList = 64 + 1024;  // per-warp candidate list (u16 items): < one round + one row
+#ifndef PHG_BP_DRAIN
+#define PHG_BP_DRAIN 3  // 2: 974.6 K, 3: 994.4 K, 4: 975.4 K (C4, measured)
+#endif
+constexpr int kBpDrain = PHG_BP_DRAIN;        // candidates per lane per drain round
+constexpr int kBpRound = 32 * kBpDrain;
+constexpr int kBpList = kBpRound + 1024;      // per-warp candidate list (u16 items): < one round + one row
 
 __host__ __device__ constexpr int bp_buf_bytes(int sh) { return (1024 * sh + 64 + 127) / 128 * 128; }
 // pad, two staged buffers, band-edge credits [warps][32][2], candidate lists [warps][kBpList]
@@ -288,18 +293,23 @@ __global__ void __launch_bounds__(kBpThreads, 2)
             return R;
         };
         unsigned pending = 0;  // warp-uniform: candidates waiting at list[0, pending)
-        // replaces the candidates list[h, h + n), n <= 64: two per lane, loads first
+        // replaces the candidates list[h, h + n), n <= kBpRound: kBpDrain per
+        // lane, all loads first
         auto drain = [&](unsigned h, unsigned n) {
-            const bool a0 = lane < n, a1 = lane + 32 < n;
-            const uint32_t o0 = lds16(list_a + 2 * (h + (a0 ? lane : 0u)));
-            const uint32_t o1 = lds16(list_a + 2 * (h + (a1 ? lane + 32u : 0u)));
-            const uint32_t v0 = bp_replace<ALE, RP>(src + o0 - RP - 1, a.k7);
-            const uint32_t v1 = bp_replace<ALE, RP>(src + o1 - RP - 1, a.k7);
-            if (a0) sts8a(dst + o0, v0);
-            if (a1) sts8a(dst + o1, v1);
+            uint32_t o[kBpDrain], v[kBpDrain];
+#pragma unroll
+            for (int u = 0; u < kBpDrain; ++u) {
+                const unsigned i = lane + 32u * u;
+                o[u] = lds16(list_a + 2 * (h + (i < n ? i : 0u)));
+            }
+#pragma unroll
+            for (int u = 0; u < kBpDrain; ++u) v[u] = bp_replace<ALE, RP>(src + o[u] - RP - 1, a.k7);
+#pragma unroll
+            for (int u = 0; u < kBpDrain; ++u)
+                if (lane + 32u * u < n) sts8a(dst + o[u], v[u]);
         };
         // appends row y's candidates R (u16 buffer offsets) at the lane's prefix
-        // in the warp list, three per loop trip; drains whole rounds of 64
+        // in the warp list, three per loop trip; drains whole rounds
         auto push = [&](uint32_t R, int y) {
             const unsigned c = __popc(R);
             unsigned incl = c;
@@ -325,18 +335,21 @@ __global__ void __launch_bounds__(kBpThreads, 2)
                 la += 6;
             }
             pending += total;
-            if (pending >= 64) {
+            if (pending >= kBpRound) {
                 __syncwarp();  // items and the destination row copies are visible
                 unsigned h = 0;
-                for (; pending - h >= 64; h += 64) drain(h, 64);
+                for (; pending - h >= kBpRound; h += kBpRound) drain(h, kBpRound);
                 pending -= h;
                 __syncwarp();
-                if (pending) {  // the leftovers (< 64) move to the front
-                    const uint32_t l0 = lane < pending ? lds16(list_a + 2 * (h + lane)) : 0u;
-                    const uint32_t l1 = lane + 32 < pending ? lds16(list_a + 2 * (h + lane + 32)) : 0u;
+                if (pending) {  // the leftovers (< kBpRound) move to the front
+                    uint32_t l[kBpDrain];
+#pragma unroll
+                    for (int u = 0; u < kBpDrain; ++u)
+                        l[u] = lane + 32u * u < pending ? lds16(list_a + 2 * (h + lane + 32u * u)) : 0u;
                     __syncwarp();
-                    if (lane < pending) sts16(list_a + 2 * lane, l0);
-                    if (lane + 32 < pending) sts16(list_a + 2 * (lane + 32), l1);
+#pragma unroll
+                    for (int u = 0; u < kBpDrain; ++u)
+                        if (lane + 32u * u < pending) sts16(list_a + 2 * (lane + 32u * u), l[u]);
                 }
                 __syncwarp();
             }
