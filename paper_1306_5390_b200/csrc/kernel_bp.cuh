@@ -61,7 +61,11 @@ constexpr int kBpPad = 128;        // dynamic smem starts with a pad (window rea
 #ifndef PHG_BP_DRAIN
 #define PHG_BP_DRAIN 3  // 2: 974.6 K, 3: 994.4 K, 4: 975.4 K (C4, measured)
 #endif
+#ifndef PHG_BP_PUSH
+#define PHG_BP_PUSH 3
+#endif
 constexpr int kBpDrain = PHG_BP_DRAIN;        // candidates per lane per drain round
+constexpr int kBpPush = PHG_BP_PUSH;          // candidates per push-loop trip
 constexpr int kBpRound = 32 * kBpDrain;
 constexpr int kBpList = kBpRound + 1024;      // per-warp candidate list (u16 items): < one round + one row
 
@@ -325,14 +329,14 @@ __global__ void __launch_bounds__(kBpThreads, 2)
             uint32_t mm = R;
             while (mm) {
 #pragma unroll
-                for (int u = 0; u < 3; ++u) {
+                for (int u = 0; u < kBpPush; ++u) {
                     uint32_t b, m1;
                     asm("bfind.u32 %0, %1;" : "=r"(b) : "r"(mm));    // ~0 once mm is empty
                     asm("shl.b32 %0, 1, %1;" : "=r"(m1) : "r"(b));   // 0 for shifts >= 32
                     if (u == 0 || mm) sts16(la + 2 * u, rowoff + bp_px(b));
                     mm ^= m1;
                 }
-                la += 6;
+                la += 2 * kBpPush;
             }
             pending += total;
             if (pending >= kBpRound) {
