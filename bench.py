@@ -287,12 +287,22 @@ class Run:
         from paper_1306_5390_b200._lib import check, lib
         self.torch, self.a, self.rank, self.local, self.world = torch, a, rank, local, world
         self.L, self.check = lib(), check
-        torch.cuda.set_device(local)
-        check(self.L.phg_set_device(local))
+        # PHG_BENCH_DEVICE / PHG_BENCH_BACKEND: a logic smoke test of the
+        # multi-rank path on a single-GPU box (every rank on one device, gloo).
+        # Never used for a reported number: ranks sharing a GPU share its time.
+        dev_idx = int(os.environ.get("PHG_BENCH_DEVICE", local))
+        backend = os.environ.get("PHG_BENCH_BACKEND", "nccl")
+        torch.cuda.set_device(dev_idx)
+        check(self.L.phg_set_device(dev_idx))
         if world > 1:
             import torch.distributed as dist
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        self.dev = torch.device("cuda", local)
+            if backend == "nccl":
+                dist.init_process_group("nccl", device_id=torch.device("cuda", dev_idx))
+            else:
+                dist.init_process_group(backend)
+        self.local = dev_idx
+        self.backend = backend
+        self.dev = torch.device("cuda", dev_idx)
         self.stream = torch.cuda.current_stream()
         self.sh = self.stream.cuda_stream
 
@@ -391,7 +401,8 @@ def step_roofline(R, src, dst, tmp, counters, params, w, rows, n, beta, k, reps,
     if os.path.exists(tpath):
         try:
             tj = json.load(open(tpath)).get(R.a.workload, {})
-            if tj.get("kernel") == name:
+            # the committed capture's launches: same kernels, same algorithmic bytes
+            if tj.get("kernel") == name and tj.get("algorithmic_bytes_per_launch") == int(alg_bytes):
                 traffic = tj.get("dram_bytes_per_launch")
         except Exception:
             pass
@@ -598,8 +609,8 @@ def run_bands(R, a):
     cfg = {"workload": "c5: " + c5_desc(a), "width": S, "height": S, "alpha": ALPHA, "beta": beta, "k": k,
            "card_threshold": 3, "border": "Faithful", "band_rows_per_rank": plan.hi - plan.lo,
            "halo_rows": beta * tmax, "launches_per_step": launches_per_step,
-           "exchange": ("nccl_p2p: dist.exchange_halos (torch.distributed batch_isend_irecv over NVLink) after "
-                        "each launch but the last, + one all_reduce of the [k,2] counters, inside the step")
+           "exchange": (f"{R.backend}_p2p: dist.exchange_halos (torch.distributed batch_isend_irecv, NVLink under "
+                        "NCCL) after each launch but the last, + one all_reduce of the [k,2] counters, inside the step")
            if R.world > 1 else "none (one rank holds the whole image)",
            "halo_exchanges_per_step": (launches_per_step - 1) if R.world > 1 else 0,
            "parallelism": f"row bands x{R.world}", "l2": "inputs larger than L2",

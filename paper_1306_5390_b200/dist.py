@@ -91,8 +91,22 @@ def exchange_halos(buf: torch.Tensor, plan: BandPlan, group=None) -> None:
         ops.append(dist.P2POp(dist.irecv, _RecvSlot(buf, plan.local(plan.hi), h).tensor, plan.down, group))
     if not ops:
         return
+    if buf.is_cuda and dist.get_backend(group) == "gloo":
+        _exchange_staged(ops)  # gloo's send/recv take host tensors (CPU multi-rank tests)
+        return
     for r in dist.batch_isend_irecv(ops):
         r.wait()
+
+
+def _exchange_staged(ops) -> None:
+    """The same P2P ops through host copies (gloo cannot send device tensors)."""
+    staged = [(op, op.tensor.cpu()) for op in ops]
+    reqs = [dist.P2POp(op.op, t, op.peer, op.group) for op, t in staged]
+    for r in dist.batch_isend_irecv(reqs):
+        r.wait()
+    for op, t in staged:
+        if op.op is dist.irecv:
+            op.tensor.copy_(t)
 
 
 class _RecvSlot:
