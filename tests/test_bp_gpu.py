@@ -125,3 +125,25 @@ def test_fp16_kernel_fallback_still_exact():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
+@pytest.mark.parametrize("w", [1, 4, 33, 300, 511, 512, 513, 700, 1024, 1025, 1500, 1992, 1993])
+def test_beta2_widths_across_layouts(w):
+    """fused_bp2_kernel (beta = 2) over the three column layouts."""
+    img = _sp(w, 41, 3 * w)
+    res = P.denoise(P.GrayImage.from_array(img), P.DenoiseParams(beta=2))
+    ref_img, ref_stats = O.denoise(img, 20, 2)
+    assert np.array_equal(res.image.pixels, ref_img), w
+    assert [(s.flagged, s.replaced) for s in res.stats] == ref_stats, w
+
+
+@pytest.mark.parametrize("h", [1, 2, 3, 4, 5, 6, 7, 9, 13, 17, 20, 21, 33, 45, 46, 100])
+@pytest.mark.parametrize("k", [1, 4, 5])
+def test_beta2_heights_bands(h, k):
+    """Row counts around the beta = 2 band split (two steps per warp at least,
+    the band-edge handover, the last warp's extra steps)."""
+    img = _sp(600, h, 11 * h + k, 0.5)
+    res = P.denoise(P.GrayImage.from_array(img), P.DenoiseParams(beta=2, max_iterations=k))
+    ref_img, ref_stats = O.denoise(img, 20, 2, k)
+    assert np.array_equal(res.image.pixels, ref_img), (h, k)
+    assert [(s.flagged, s.replaced) for s in res.stats] == ref_stats, (h, k)
