@@ -354,23 +354,25 @@ class Run:
         return ms, launches, clk.summary()
 
 
-def plan_of(L, k, beta):
-    tmax = L.phg_max_fused_iterations(beta)
-    if tmax <= 0:
-        return [1] * k
-    n = -(-k // tmax)
-    return [k // n + (1 if i < k % n else 0) for i in range(n)]
+def plan_of(L, params):
+    """The fused launches of one step, as the library plans them (phg_launch_plan)."""
+    buf = (C.c_int * 64)()
+    n = L.phg_launch_plan(C.byref(params), buf, 64)
+    if n < 0:
+        raise RuntimeError(L.phg_last_error().decode())
+    return list(buf[:n])
 
 
 def step_roofline(R, src, dst, tmp, counters, params, w, rows, n, beta, k, reps, row_base=0, height=None,
                   own=None):
-    """The launches of ONE step (the k-plan of fused launches, e.g. T=5 for
-    beta=1, T=3 + T=2 for beta=2), timed back to back on the launching stream
-    with CUDA events; roofline record against the measured HBM peak."""
+    """The launches of ONE step (the library's launch plan: one T=5 launch for
+    beta=1, five T=1 launches for beta=2), timed back to back on the launching
+    stream with CUDA events; roofline record against the measured HBM peak."""
     torch, L = R.torch, R.L
     height = height or rows
     own_lo, own_hi = own or (0, height)
-    plan = plan_of(L, k, beta)
+    plan = plan_of(L, params)
+    k = sum(plan)
     bufs = [src, dst, tmp]
 
     def one_step():
@@ -395,7 +397,8 @@ def step_roofline(R, src, dst, tmp, counters, params, w, rows, n, beta, k, reps,
     peak, peak_src = peaks()
     achieved = alg_bytes / (k_ms / 1e3) / 1e9
     names = [L.phg_fused_kernel_name(C.byref(params), T).decode() for T in plan]
-    name = names[0] if len(set(names)) == 1 and len(names) == 1 else " + ".join(names)
+    name = names[0] if len(names) == 1 else (f"{len(names)} x {names[0]}" if len(set(names)) == 1
+                                             else " + ".join(names))
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
@@ -574,7 +577,8 @@ def run_bands(R, a):
     src = dev_image(bufs[0], S, plan.rows, 1)
     dst = dev_image(bufs[1], S, plan.rows, 1)
     tmp = dev_image(bufs[2], S, plan.rows, 1)
-    roof = step_roofline(R, src, dst, tmp, counters, params, S, plan.rows, 1, beta, min(k, tmax),
+    roof = step_roofline(R, src, dst, tmp, counters, PhgParams(ALPHA, beta, min(k, tmax), 3, 0), S, plan.rows, 1,
+                         beta, min(k, tmax),
                          max(5, min(a.steps, 10)), row_base=plan.blo, height=S, own=(plan.lo, plan.hi))
     host_out = torch.empty((plan.hi - plan.lo, S), dtype=torch.uint8, pin_memory=True)
 

@@ -157,6 +157,13 @@ typedef struct phg_dev_image {
  * (temporal blocking depth; 0 if beta has no fused kernel). */
 int phg_max_fused_iterations(int beta);
 
+/* The launches a denoise with these parameters runs: fills iters_per_launch
+ * (capacity cap) with the iterations of each fused launch and returns their
+ * number (e.g. k = 5: {5} for beta = 1, {1,1,1,1,1} for the beta = 2 default
+ * kernel, whose temporal blocking does not pay); negative on error.  With
+ * iters_per_launch == NULL only the count is returned. */
+int phg_launch_plan(const phg_params* p, int* iters_per_launch, int cap);
+
 /* Name of the kernel one fused launch of `iters` iterations runs for these
  * parameters (static string; "" if none).  For reports and profiles. */
 const char* phg_fused_kernel_name(const phg_params* p, int iters);

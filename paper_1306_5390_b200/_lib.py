@@ -26,6 +26,7 @@ EXPORTS = (
     "phg_fused_kernel_name", "phg_residual_noise_count", "phg_sse", "phg_dev_residual_count", "phg_dev_sse",
     "phg_dev_synth_smooth", "phg_dev_inject_noise", "phg_denoise_sharded", "phg_dev_fused_step_mirrored",
     "phg_ipc_get_handle", "phg_ipc_open_handle", "phg_ipc_close", "phg_debug_rms", "phg_denoise_pgm_file",
+    "phg_launch_plan",
 )
 
 
@@ -113,6 +114,7 @@ def lib():
         L.phg_finalize_stats.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(PhgPassStats),
                                          C.POINTER(C.c_int)]
         L.phg_max_fused_iterations.argtypes = [C.c_int]
+        L.phg_launch_plan.argtypes = [C.POINTER(PhgParams), C.c_void_p, C.c_int]
         L.phg_fused_kernel_name.argtypes = [C.POINTER(PhgParams), C.c_int]
         L.phg_fused_kernel_name.restype = C.c_char_p
         L.phg_residual_noise_count.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,

@@ -654,13 +654,26 @@ int step(const phg_dev_image& src, const phg_dev_image& dst, int row_base, int h
                          own_hi, p, it0, counters, kcap, stream, peers);
 }
 
-// Split k iterations into launches of at most max_fused(beta), evenly.
-std::vector<int> chunk_plan(int k, int beta) {
+// Iterations per launch: the kernel's maximum, except for the beta = 2
+// packed-bit kernel, whose temporal blocking costs more in halo rows (2 per
+// side and iteration) than it saves in HBM traffic -- C3, k = 5: T3+T2
+// 676 K, T2+T2+T1 700 K, five T1 launches 714 K Mpix-it/s (measured).
+// `deep`: paths that pay per launch (the row-pipelined host path, whose
+// wavefront grows with the launch count -- C3 e2e 181 K with T3+T2, 150 K
+// with five T1 -- and the band engines, which exchange halos per launch)
+// keep the deepest blocking.
+int launch_depth(const phg_params& p, bool deep) {
     static const int cap = [] {
         const char* e = getenv("PHG_TMAX");  // temporal-blocking depth cap (tuning)
         return e ? std::max(1, atoi(e)) : 1 << 20;
     }();
-    const int tmax = std::max(1, std::min(cap, max_fused(beta)));
+    const int pref = (!deep && use_bp2(p, 1)) ? 1 : max_fused(p.beta);
+    return std::max(1, std::min(cap, pref));
+}
+
+// Split k iterations into launches of at most launch_depth(p, deep), evenly.
+std::vector<int> chunk_plan(int k, const phg_params& p, bool deep = false) {
+    const int tmax = launch_depth(p, deep);
     const int n = (k + tmax - 1) / tmax;
     std::vector<int> c(n, k / n);
     for (int i = 0; i < k % n; ++i) ++c[i];
@@ -844,7 +857,7 @@ int denoise_bands(DeviceState* s, const phg_dev_image& in, int w, int h, const p
         const int hi = static_cast<int>(static_cast<int64_t>(h) * (k + 1) / nbands);
         if (hi > lo) bands.push_back({lo, hi, 0, 0, {}, {}});
     }
-    const std::vector<int> plan = chunk_plan(p.max_iterations, p.beta);
+    const std::vector<int> plan = chunk_plan(p.max_iterations, p, true);
     const int tmax = *std::max_element(plan.begin(), plan.end());
     const int halo = p.beta * tmax;
     int slot = 8;
@@ -943,6 +956,17 @@ int phg_set_device(int device) {
 }
 
 int phg_max_fused_iterations(int beta) { return max_fused(beta); }
+
+int phg_launch_plan(const phg_params* p, int* iters_per_launch, int cap) {
+    PHG_TRY(validate(p));
+    const std::vector<int> plan =
+        max_fused(p->beta) > 0 ? chunk_plan(p->max_iterations, *p) : std::vector<int>(p->max_iterations, 1);
+    if (iters_per_launch) {
+        if (cap < static_cast<int>(plan.size())) return fail(PHG_EINVAL, "launch plan capacity too small");
+        std::copy(plan.begin(), plan.end(), iters_per_launch);
+    }
+    return static_cast<int>(plan.size());
+}
 
 const char* phg_fused_kernel_name(const phg_params* p, int iters) {
     static const char* const h2[] = {"", "fused_h2_kernel<T=1>", "fused_h2_kernel<T=2>", "fused_h2_kernel<T=3>",
@@ -1077,7 +1101,7 @@ int phg_dev_denoise(const phg_dev_image* src, const phg_dev_image* dst, const ph
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int k = p->max_iterations;
     PHG_CUDA(cudaMemsetAsync(counters, 0, sizeof(uint64_t) * 2 * k * src->n_images, st));
-    const std::vector<int> plan = max_fused(p->beta) > 0 ? chunk_plan(k, p->beta) : std::vector<int>(k, 1);
+    const std::vector<int> plan = max_fused(p->beta) > 0 ? chunk_plan(k, *p) : std::vector<int>(k, 1);
     const int nl = static_cast<int>(plan.size());
     const phg_dev_image* cur = src;
     int it0 = 0;
@@ -1395,7 +1419,7 @@ int phg_denoise_pass(const uint8_t* img, int w, int h, const int32_t* card, int 
 int denoise_rows_pipelined(DeviceState* s, const uint8_t* img, int w, int h, const phg_params& p, uint8_t* out,
                            uint64_t* ctr, int nchunks, int npieces) {
     const int k = p.max_iterations;
-    const std::vector<int> plan = chunk_plan(k, p.beta);
+    const std::vector<int> plan = chunk_plan(k, p, true);
     const int L = static_cast<int>(plan.size());
     const int64_t pitch = round_up(w, 16), img_bytes = static_cast<int64_t>(w) * h;
     void *pin, *pout, *pa, *pb, *pc;
@@ -1527,7 +1551,7 @@ void row_plan_for(int w, int h, int halo, int& nchunks, int& npieces) {
 }
 
 int pipeline_halo(const phg_params& p) {
-    const std::vector<int> plan = chunk_plan(p.max_iterations, p.beta);
+    const std::vector<int> plan = chunk_plan(p.max_iterations, p, true);
     return p.beta * (max_fused(p.beta) > 0 ? *std::max_element(plan.begin(), plan.end()) : 1);
 }
 
@@ -1732,7 +1756,7 @@ struct ShardBand {
 int sharded_bands(const uint8_t* img, int w, int h, const phg_params& p, const int* devices, int ndev,
                   uint8_t* out, phg_pass_stats* stats, int* iterations_run) {
     const int k = p.max_iterations;
-    const std::vector<int> plan = chunk_plan(k, p.beta);
+    const std::vector<int> plan = chunk_plan(k, p, true);
     const int halo = p.beta * *std::max_element(plan.begin(), plan.end());
     const int64_t pitch = round_up(w, 16);
     std::vector<ShardBand> bands;
