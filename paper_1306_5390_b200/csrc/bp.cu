@@ -36,7 +36,11 @@ BpFn pick2(bool ale, bool wide) {
     return ale ? fused_bp2_kernel<T, true, false> : fused_bp2_kernel<T, false, false>;
 }
 
-BpFn select2(int T, bool ale, bool wide) {
+BpFn select2(int T, bool ale, bool wide, bool direct) {
+    if (direct) {
+        if (T != 1 || !wide) return nullptr;
+        return ale ? fused_bp2_kernel<1, true, true, true> : fused_bp2_kernel<1, false, true, true>;
+    }
     switch (T) {
         case 1: return pick2<1>(ale, wide);
         case 2: return pick2<2>(ale, wide);
@@ -48,20 +52,20 @@ BpFn select2(int T, bool ale, bool wide) {
 
 }  // namespace
 
-cudaError_t launch_bp2_kernel(int T, bool ale, bool wide, const CUtensorMap& map, const BpArgs& a, unsigned grid,
-                              size_t smem, cudaStream_t stream) {
-    BpFn fn = select2(T, ale, wide);
+cudaError_t launch_bp2_kernel(int T, bool ale, bool wide, bool direct, const CUtensorMap& map, const BpArgs& a,
+                              unsigned grid, size_t smem, cudaStream_t stream) {
+    BpFn fn = select2(T, ale, wide, direct);
     if (!fn) return cudaErrorInvalidValue;
-    if (smem > bp2_smem(kBp2MaxRows)) return cudaErrorInvalidValue;
+    const size_t cap = direct ? bp2_smem(kBp2DirectMaxRows, true) : bp2_smem(kBp2MaxRows);
+    if (smem > cap) return cudaErrorInvalidValue;
     cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(bp2_smem(kBp2MaxRows)));
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cap));
     if (e != cudaSuccess) return e;
     fn<<<grid, kBpThreads, smem, stream>>>(map, a);
     return cudaGetLastError();
 }
 
-size_t bp2_smem(int sh) { return static_cast<size_t>(bp2_smem_bytes(sh)); }
+size_t bp2_smem(int sh, bool direct) { return static_cast<size_t>(bp2_smem_bytes(sh, direct)); }
 
 cudaError_t launch_bp_kernel(int T, bool ale, bool wide, const CUtensorMap& map, const BpArgs& a, unsigned grid,
                              size_t smem, cudaStream_t stream) {

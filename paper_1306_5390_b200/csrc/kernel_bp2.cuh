@@ -29,6 +29,14 @@
 //
 // Candidates are replaced exactly as for beta = 1 (per-warp list, balanced
 // rounds of 64) with the 5x5 window: f = 24 - #similar in {23, 24}.
+//
+// DIRECT (T = 1, wide regions, no peer mirrors): one iteration per launch
+// needs no second staged buffer -- each owned row goes straight from the sweep
+// to HBM (two 16-byte stores per lane) and each replaced pixel is stored to
+// HBM by the drain (the warp's own rows; __syncwarp orders it after the row
+// store).  One buffer doubles the tile height (90 staged rows), halving the
+// per-tile halo and fixed costs, and the output store loop disappears.
+// List items are then band-relative ((row - b0) * 1024 + column).
 #pragma once
 #include <cuda.h>
 #include <cstdint>
@@ -37,8 +45,8 @@
 
 namespace phg {
 
-__host__ __device__ constexpr int bp2_smem_bytes(int sh) {
-    return kBpPad + 2 * bp_buf_bytes(sh) + kBpWarps * 32 * 16 + kBpWarps * kBpList * 2;
+__host__ __device__ constexpr int bp2_smem_bytes(int sh, bool direct = false) {
+    return kBpPad + (direct ? 1 : 2) * bp_buf_bytes(sh) + kBpWarps * 32 * 16 + kBpWarps * kBpList * 2;
 }
 
 // packed masks shifted by +-1, +-2 pixels along the strip (bit of pixel q
@@ -129,10 +137,11 @@ __device__ __forceinline__ uint32_t bp2_replace(uint32_t o1, uint32_t k7) {
     return h2_rms(S, f, rcp);
 }
 
-template <int T, bool ALE, bool WIDE>
+template <int T, bool ALE, bool WIDE, bool DIRECT = false>
 __global__ void __launch_bounds__(kBpThreads, 2)
     fused_bp2_kernel(const __grid_constant__ CUtensorMap src_map, const BpArgs a) {
     static_assert(T >= 1 && T <= 8, "halo exceeds the aprons");
+    static_assert(!DIRECT || (T == 1 && WIDE), "direct stores: one iteration, wide regions");
     constexpr int HALO = 2 * T;
     constexpr int RP = WIDE ? 1024 : 512;
     constexpr int NH = WIDE ? 1 : 2;
@@ -147,7 +156,7 @@ __global__ void __launch_bounds__(kBpThreads, 2)
     const int lane = tid & 31;
     const int warp = tid >> 5;
     const uint32_t s0 = smem_u32(smem);
-    const uint32_t down_a = s0 + 2 * bufb;  // [warps][32][4] u32: rows b1-2, b1-1 of the band above, (o, w)
+    const uint32_t down_a = s0 + (DIRECT ? 1 : 2) * bufb;  // [warps][32][4] u32: rows b1-2, b1-1 of the band above, (o, w)
     const uint32_t list_a = down_a + kBpWarps * 32 * 16 + warp * kBpList * 2;
     const uint32_t half_bytes = static_cast<uint32_t>(sh) * 512u;
 
@@ -218,6 +227,12 @@ __global__ void __launch_bounds__(kBpThreads, 2)
     auto rowint = [&](int y) { return static_cast<unsigned>(y - ilo) < static_cast<unsigned>(ihi - ilo); };
     auto rowown = [&](int y) { return static_cast<unsigned>(y - HALO) < static_cast<unsigned>(myout); };
     const int west = (lane + 31) & 31, east = (lane + 1) & 31;
+    // DIRECT: global offset of the tile's buffer row 0, region column 0, and
+    // which of the lane's two 16-px chunks are output columns
+    const int64_t gtile = static_cast<int64_t>(imgA) * a.image_stride + static_cast<int64_t>(y0A) * a.pitch + x0A;
+    const int px0 = lane * 32;
+    const bool own0 = px0 >= a.x_apron && px0 < a.x_apron + a.x_step && x0A + px0 < W;
+    const bool own1 = px0 + 16 >= a.x_apron && px0 + 16 < a.x_apron + a.x_step && x0A + px0 + 16 < W;
 
     __syncthreads();
     mbar_wait(&bar, 0);
@@ -241,17 +256,27 @@ __global__ void __launch_bounds__(kBpThreads, 2)
                 fl += __popc(F & cOwn);
                 rp += __popc(R & cOwn);
             }
-            return R;
+            // DIRECT: nothing reads the value of a pixel this tile does not
+            // own, so only owned candidates are replaced
+            return DIRECT ? (rowown(y) ? R & cOwn : 0u) : R;
         };
         unsigned pending = 0;
+        // DIRECT items are relative to the band's first row
+        const uint32_t ibase = DIRECT ? static_cast<uint32_t>(b0) * RP : 0u;
+        uint8_t* const gband = a.dst + gtile + static_cast<int64_t>(b0) * a.pitch;
         auto drain = [&](unsigned h, unsigned nn) {
             const bool a0 = lane < nn, a1 = lane + 32 < nn;
             const uint32_t o0 = lds16(list_a + 2 * (h + (a0 ? lane : 0u)));
             const uint32_t o1 = lds16(list_a + 2 * (h + (a1 ? lane + 32u : 0u)));
-            const uint32_t v0 = bp2_replace<ALE, RP>(src + o0 - 2 * RP - 2, a.k7);
-            const uint32_t v1 = bp2_replace<ALE, RP>(src + o1 - 2 * RP - 2, a.k7);
-            if (a0) sts8a(dst + o0, v0);
-            if (a1) sts8a(dst + o1, v1);
+            const uint32_t v0 = bp2_replace<ALE, RP>(src + ibase + o0 - 2 * RP - 2, a.k7);
+            const uint32_t v1 = bp2_replace<ALE, RP>(src + ibase + o1 - 2 * RP - 2, a.k7);
+            if constexpr (DIRECT) {
+                if (a0) gband[static_cast<int64_t>(o0 >> 10) * a.pitch + (o0 & 1023u)] = static_cast<uint8_t>(v0);
+                if (a1) gband[static_cast<int64_t>(o1 >> 10) * a.pitch + (o1 & 1023u)] = static_cast<uint8_t>(v1);
+            } else {
+                if (a0) sts8a(dst + o0, v0);
+                if (a1) sts8a(dst + o1, v1);
+            }
         };
         auto push = [&](uint32_t R, int y) {
             const unsigned c = __popc(R);
@@ -264,7 +289,7 @@ __global__ void __launch_bounds__(kBpThreads, 2)
             const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
             if (total == 0) return;
             uint32_t la = list_a + 2 * (pending + incl - c);
-            const uint32_t rowoff = cb + static_cast<uint32_t>(y) * RP;
+            const uint32_t rowoff = cb + static_cast<uint32_t>(y) * RP - ibase;
             uint32_t mm = R;
             while (mm) {
 #pragma unroll
@@ -334,7 +359,13 @@ __global__ void __launch_bounds__(kBpThreads, 2)
                 cX = om_add(cX, Om{bp_shW1(gm1.o, east), bp_shW1(gm1.w, east)});
                 cX = om_add(cX, Om{bp_shW2(gm2.o, east), bp_shW2(gm2.w, east)});
                 // the unchanged row goes to the destination
-                if (r < hi) {
+                if constexpr (DIRECT) {
+                    if (rowown(r)) {
+                        uint8_t* g = a.dst + gtile + static_cast<int64_t>(r) * a.pitch + px0;
+                        if (own0) *reinterpret_cast<uint4*>(g) = make_uint4(X[0], X[1], X[2], X[3]);
+                        if (own1) *reinterpret_cast<uint4*>(g + 16) = make_uint4(X[4], X[5], X[6], X[7]);
+                    }
+                } else if (r < hi) {
                     const uint32_t da = dst + cb + r * RP;
                     sts128a(da, make_uint4(X[0], X[1], X[2], X[3]));
                     sts128a(da + 16, make_uint4(X[4], X[5], X[6], X[7]));
@@ -391,7 +422,8 @@ __global__ void __launch_bounds__(kBpThreads, 2)
         __syncthreads();
     }
 
-    {
+    // the staged (DIRECT: only when the iteration was skipped) or final rows
+    if (!DIRECT || nit == 0) {
         const uint8_t* fin = smem + ((nit & 1) ? bufb : 0);
         constexpr int kChunksRow = RP / 16;
         const int c_lo = a.x_apron / 16;

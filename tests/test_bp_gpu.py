@@ -147,3 +147,55 @@ def test_beta2_heights_bands(h, k):
     ref_img, ref_stats = O.denoise(img, 20, 2, k)
     assert np.array_equal(res.image.pixels, ref_img), (h, k)
     assert [(s.flagged, s.replaced) for s in res.stats] == ref_stats, (h, k)
+
+
+# ---- the single-buffer beta = 2 form (DIRECT: T = 1 launches of the resident
+# path on wide regions store rows and replaced pixels straight to HBM; tiles
+# of up to 90 staged rows, band-relative candidate items)
+
+def _check2(img, alpha=20, k=5, thr=3):
+    res = P.denoise(P.GrayImage.from_array(img), P.DenoiseParams(alpha, 2, k, thr))
+    ref_img, ref_stats = O.denoise(img, alpha, 2, k, thr, 0)
+    assert np.array_equal(res.image.pixels, ref_img), (img.shape, alpha, k, thr)
+    assert [(s.flagged, s.replaced) for s in res.stats] == ref_stats, (img.shape, alpha, k, thr)
+
+
+@pytest.mark.parametrize("w,h", [(600, 86), (600, 87), (1025, 181), (2100, 300), (3000, 95), (1993, 173)])
+@pytest.mark.parametrize("k", [1, 3])
+def test_beta2_direct_tiles(w, h, k):
+    """Row tiles around the 86-row output height, column tiles with aprons."""
+    _check2(_sp(w, h, w + h + k, 0.5), k=k)
+
+
+@pytest.mark.parametrize("alpha", [1, 30, 128, 129, 200])
+def test_beta2_direct_dense_candidates(alpha):
+    """Uniform-random pixels: whole rows of candidates in the band-relative
+    list (rounds of 64, leftovers), both similarity forms (alpha <= 128 and
+    > 128)."""
+    rng = np.random.default_rng(alpha)
+    _check2(rng.integers(0, 256, (190, 1500), dtype=np.uint8), alpha=alpha, k=2)
+
+
+@pytest.mark.parametrize("thr", [1, 2, 3])
+def test_beta2_direct_thresholds(thr):
+    _check2(_sp(1100, 120, thr, 0.4), k=4, thr=thr)
+
+
+def test_beta2_direct_early_exit():
+    """A converged image (constant + 1% noise) at k = 64: after the fixed
+    point the direct launches only copy the staged rows."""
+    n = O.inject_sp_noise(np.full((200, 1500), 128, np.uint8), 0.01, 0.5, 9)
+    _check2(n, k=64)
+
+
+def test_beta2_direct_off_switch_same_result():
+    """PHG_NO_BP2_DIRECT=1 keeps the two-buffer T = 1 form; both agree."""
+    code = ("import numpy as np, paper_1306_5390_b200 as P; from oracle import oracle as O;"
+            "n=O.inject_sp_noise(O.synth_image(1500,200,5),0.5,0.5,6);"
+            "r=P.denoise(P.GrayImage.from_array(n),P.DenoiseParams(beta=2));"
+            "i,s=O.denoise(n,20,2); assert np.array_equal(r.image.pixels,i); "
+            "assert [(x.flagged,x.replaced) for x in r.stats]==s; print('ok')")
+    env = dict(os.environ, PHG_NO_BP2_DIRECT="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
