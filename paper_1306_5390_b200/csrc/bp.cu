@@ -19,7 +19,11 @@ BpFn pick(bool ale, bool wide) {
     return ale ? fused_bp_kernel<T, true, false> : fused_bp_kernel<T, false, false>;
 }
 
-BpFn select(int T, bool ale, bool wide) {
+BpFn select(int T, bool ale, bool wide, bool direct) {
+    if (direct) {
+        if (T != 1 || !wide) return nullptr;
+        return ale ? fused_bp_kernel<1, true, true, true> : fused_bp_kernel<1, false, true, true>;
+    }
     switch (T) {
         case 1: return pick<1>(ale, wide);
         case 2: return pick<2>(ale, wide);
@@ -67,21 +71,21 @@ cudaError_t launch_bp2_kernel(int T, bool ale, bool wide, bool direct, const CUt
 
 size_t bp2_smem(int sh, bool direct) { return static_cast<size_t>(bp2_smem_bytes(sh, direct)); }
 
-cudaError_t launch_bp_kernel(int T, bool ale, bool wide, const CUtensorMap& map, const BpArgs& a, unsigned grid,
-                             size_t smem, cudaStream_t stream) {
-    BpFn fn = select(T, ale, wide);
+cudaError_t launch_bp_kernel(int T, bool ale, bool wide, bool direct, const CUtensorMap& map, const BpArgs& a,
+                             unsigned grid, size_t smem, cudaStream_t stream) {
+    BpFn fn = select(T, ale, wide, direct);
     if (!fn) return cudaErrorInvalidValue;
     // always the largest tile's size: concurrent callers with different tile
     // heights must never lower the limit under another caller's launch
-    if (smem > bp_smem(kBpMaxRows)) return cudaErrorInvalidValue;
+    const size_t cap = direct ? bp_smem(kBpDirectMaxRows, true) : bp_smem(kBpMaxRows);
+    if (smem > cap) return cudaErrorInvalidValue;
     cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(bp_smem(kBpMaxRows)));
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cap));
     if (e != cudaSuccess) return e;
     fn<<<grid, kBpThreads, smem, stream>>>(map, a);
     return cudaGetLastError();
 }
 
-size_t bp_smem(int sh) { return static_cast<size_t>(bp_smem_bytes(sh)); }
+size_t bp_smem(int sh, bool direct) { return static_cast<size_t>(bp_smem_bytes(sh, direct)); }
 
 }  // namespace phg

@@ -13,6 +13,7 @@ namespace phg {
 constexpr int kBpMaxRows = 46;   // staged rows: two CTAs per SM (beta = 1)
 constexpr int kBp2MaxRows = 45;  // beta = 2 (larger band-edge handover)
 constexpr int kBp2DirectMaxRows = 90;  // beta = 2, one iteration, one staged buffer
+constexpr int kBpDirectMaxRows = 92;   // beta = 1, one iteration, one staged buffer
 
 struct BpArgs {
     uint8_t* dst;
@@ -40,11 +41,11 @@ struct BpArgs {
     HaloPeers peers;               // single-image bands only (kernels.cuh)
 };
 
-// Launches fused_bp_kernel<T, alpha <= 128, wide> with `grid` CTAs.
-cudaError_t launch_bp_kernel(int T, bool ale, bool wide, const CUtensorMap& map, const BpArgs& a, unsigned grid,
-                             size_t smem, cudaStream_t stream);
+// Launches fused_bp_kernel<T, alpha <= 128, wide[, direct]> with `grid` CTAs.
+cudaError_t launch_bp_kernel(int T, bool ale, bool wide, bool direct, const CUtensorMap& map, const BpArgs& a,
+                             unsigned grid, size_t smem, cudaStream_t stream);
 // dynamic shared memory of one CTA staging sh rows
-size_t bp_smem(int sh);
+size_t bp_smem(int sh, bool direct = false);
 // the beta = 2 kernel (kernel_bp2.cuh), T <= 4; `direct`: the single-buffer
 // T = 1 form that stores straight to HBM (wide regions, no peer mirrors)
 cudaError_t launch_bp2_kernel(int T, bool ale, bool wide, bool direct, const CUtensorMap& map, const BpArgs& a,

@@ -70,9 +70,10 @@ constexpr int kBpRound = 32 * kBpDrain;
 constexpr int kBpList = kBpRound + 1024;      // per-warp candidate list (u16 items): < one round + one row
 
 __host__ __device__ constexpr int bp_buf_bytes(int sh) { return (1024 * sh + 64 + 127) / 128 * 128; }
-// pad, two staged buffers, band-edge credits [warps][32][2], candidate lists [warps][kBpList]
-__host__ __device__ constexpr int bp_smem_bytes(int sh) {
-    return kBpPad + 2 * bp_buf_bytes(sh) + kBpWarps * 32 * 8 + kBpWarps * kBpList * 2;
+// pad, two staged buffers (DIRECT: one), band-edge credits [warps][32][2],
+// candidate lists [warps][kBpList]
+__host__ __device__ constexpr int bp_smem_bytes(int sh, bool direct = false) {
+    return kBpPad + (direct ? 1 : 2) * bp_buf_bytes(sh) + kBpWarps * 32 * 8 + kBpWarps * kBpList * 2;
 }
 
 
@@ -181,10 +182,13 @@ __device__ __forceinline__ uint32_t bp_replace(uint32_t o1, uint32_t k7) {
     return h2_rms(S, f, rcp);
 }
 
-template <int T, bool ALE, bool WIDE>
+// DIRECT (T = 1, wide regions, no peer mirrors): one staged buffer; owned
+// rows and replaced pixels are stored straight to HBM (see kernel_bp2.cuh).
+template <int T, bool ALE, bool WIDE, bool DIRECT = false>
 __global__ void __launch_bounds__(kBpThreads, 2)
     fused_bp_kernel(const __grid_constant__ CUtensorMap src_map, const BpArgs a) {
     static_assert(T >= 1 && T <= 8, "halo exceeds the aprons");
+    static_assert(!DIRECT || (T == 1 && WIDE), "direct stores: one iteration, wide regions");
     constexpr int HALO = T;
     constexpr int RP = WIDE ? 1024 : 512;  // staged row pitch of one tile
     constexpr int NH = WIDE ? 1 : 2;       // tiles per CTA
@@ -199,7 +203,7 @@ __global__ void __launch_bounds__(kBpThreads, 2)
     const int lane = tid & 31;
     const int warp = tid >> 5;
     const uint32_t s0 = smem_u32(smem);
-    const uint32_t down_a = s0 + 2 * bufb;            // [warps][32][2] u32 band-edge credits
+    const uint32_t down_a = s0 + (DIRECT ? 1 : 2) * bufb;  // [warps][32][2] u32 band-edge credits
     const uint32_t list_a = down_a + kBpWarps * 32 * 8 + warp * kBpList * 2;  // this warp's u16 list
     const uint32_t half_bytes = static_cast<uint32_t>(sh) * 512u;  // narrow: tile B offset
 
@@ -271,6 +275,12 @@ __global__ void __launch_bounds__(kBpThreads, 2)
     auto rowint = [&](int y) { return static_cast<unsigned>(y - ilo) < static_cast<unsigned>(ihi - ilo); };
     auto rowown = [&](int y) { return static_cast<unsigned>(y - HALO) < static_cast<unsigned>(myout); };
     const int west = (lane + 31) & 31;
+    // DIRECT: global offset of the tile's buffer row 0, region column 0, and
+    // which of the lane's two 16-px chunks are output columns
+    const int64_t gtile = static_cast<int64_t>(imgA) * a.image_stride + static_cast<int64_t>(y0A) * a.pitch + x0A;
+    const int px0 = lane * 32;
+    const bool own0 = px0 >= a.x_apron && px0 < a.x_apron + a.x_step && x0A + px0 < W;
+    const bool own1 = px0 + 16 >= a.x_apron && px0 + 16 < a.x_apron + a.x_step && x0A + px0 + 16 < W;
 
     __syncthreads();  // barrier init + counters visible
     mbar_wait(&bar, 0);
@@ -294,11 +304,15 @@ __global__ void __launch_bounds__(kBpThreads, 2)
                 fl += __popc(F & cOwn);
                 rp += __popc(R & cOwn);
             }
-            return R;
+            // DIRECT: only owned candidates (nothing reads the others)
+            return DIRECT ? (rowown(y) ? R & cOwn : 0u) : R;
         };
         unsigned pending = 0;  // warp-uniform: candidates waiting at list[0, pending)
         // replaces the candidates list[h, h + n), n <= kBpRound: kBpDrain per
         // lane, all loads first
+        // DIRECT items are relative to the band's first row
+        const uint32_t ibase = DIRECT ? static_cast<uint32_t>(b0) * RP : 0u;
+        uint8_t* const gband = a.dst + gtile + static_cast<int64_t>(b0) * a.pitch;
         auto drain = [&](unsigned h, unsigned n) {
             uint32_t o[kBpDrain], v[kBpDrain];
 #pragma unroll
@@ -307,10 +321,15 @@ __global__ void __launch_bounds__(kBpThreads, 2)
                 o[u] = lds16(list_a + 2 * (h + (i < n ? i : 0u)));
             }
 #pragma unroll
-            for (int u = 0; u < kBpDrain; ++u) v[u] = bp_replace<ALE, RP>(src + o[u] - RP - 1, a.k7);
+            for (int u = 0; u < kBpDrain; ++u) v[u] = bp_replace<ALE, RP>(src + ibase + o[u] - RP - 1, a.k7);
 #pragma unroll
             for (int u = 0; u < kBpDrain; ++u)
-                if (lane + 32u * u < n) sts8a(dst + o[u], v[u]);
+                if (lane + 32u * u < n) {
+                    if constexpr (DIRECT)
+                        gband[static_cast<int64_t>(o[u] >> 10) * a.pitch + (o[u] & 1023u)] = static_cast<uint8_t>(v[u]);
+                    else
+                        sts8a(dst + o[u], v[u]);
+                }
         };
         // appends row y's candidates R (u16 buffer offsets) at the lane's prefix
         // in the warp list, three per loop trip; drains whole rounds
@@ -325,7 +344,7 @@ __global__ void __launch_bounds__(kBpThreads, 2)
             const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
             if (total == 0) return;
             uint32_t la = list_a + 2 * (pending + incl - c);
-            const uint32_t rowoff = cb + static_cast<uint32_t>(y) * RP;
+            const uint32_t rowoff = cb + static_cast<uint32_t>(y) * RP - ibase;
             uint32_t mm = R;
             while (mm) {
 #pragma unroll
@@ -392,9 +411,17 @@ __global__ void __launch_bounds__(kBpThreads, 2)
                 const uint32_t w = wA | wB | (oA & oB), o = oA | oB;
                 // the unchanged row goes to the destination (candidates are
                 // overwritten by the replacement)
-                const uint32_t da = dst + cb + y * RP;
-                sts128a(da, make_uint4(X[0], X[1], X[2], X[3]));
-                sts128a(da + 16, make_uint4(X[4], X[5], X[6], X[7]));
+                if constexpr (DIRECT) {
+                    if (rowown(y)) {
+                        uint8_t* g = a.dst + gtile + static_cast<int64_t>(y) * a.pitch + px0;
+                        if (own0) *reinterpret_cast<uint4*>(g) = make_uint4(X[0], X[1], X[2], X[3]);
+                        if (own1) *reinterpret_cast<uint4*>(g + 16) = make_uint4(X[4], X[5], X[6], X[7]);
+                    }
+                } else {
+                    const uint32_t da = dst + cb + y * RP;
+                    sts128a(da, make_uint4(X[0], X[1], X[2], X[3]));
+                    sts128a(da + 16, make_uint4(X[4], X[5], X[6], X[7]));
+                }
                 if (y == b0) {
                     of = o;
                     wf = w;
@@ -464,8 +491,9 @@ __global__ void __launch_bounds__(kBpThreads, 2)
         }
     }
 
-    // ---- owned output rows: 16-byte coalesced stores
-    {
+    // ---- owned output rows: 16-byte coalesced stores (DIRECT: only when
+    // the iteration was skipped -- the staged rows are the result)
+    if (!DIRECT || nit == 0) {
         const uint8_t* fin = smem + ((nit & 1) ? bufb : 0);
         constexpr int kChunksRow = RP / 16;
         const int c_lo = a.x_apron / 16;

@@ -368,17 +368,19 @@ int launch_bp(const phg_dev_image& src, const phg_dev_image& dst, int row_base, 
     const bool b2 = p.beta == 2;
     const int halo = p.beta * iters;
     const BpCols cols = bp_cols(src.width);
-    // beta = 2, one iteration: the single-buffer form (direct HBM stores)
-    // unless the band engine mirrors rows to peers
-    static const bool no_direct = getenv("PHG_NO_BP2_DIRECT") != nullptr;
-    const bool direct = b2 && iters == 1 && cols.wide && !no_direct && peers.ptr[0] == nullptr &&
-                        peers.ptr[1] == nullptr;
-    const int max_rows = direct ? phg::kBp2DirectMaxRows : b2 ? phg::kBp2MaxRows : phg::kBpMaxRows;
+    // one iteration on wide regions: the single-buffer form (direct HBM
+    // stores) unless the band engine mirrors rows to peers.  (Storing the
+    // last iteration of a T = 5 launch straight to HBM instead of through the
+    // output loop measured slower: C4 918 vs 994 K, C5 1069 vs 1124 K.)
+    static const bool no_direct = getenv("PHG_NO_DIRECT") != nullptr;
+    const bool direct = iters == 1 && cols.wide && !no_direct && peers.ptr[0] == nullptr && peers.ptr[1] == nullptr;
+    const int max_rows = direct ? (b2 ? phg::kBp2DirectMaxRows : phg::kBpDirectMaxRows)
+                                : (b2 ? phg::kBp2MaxRows : phg::kBpMaxRows);
     const int target = direct ? max_rows : std::min(bp_rows_target(), max_rows);
     const Launch L = plan_rows_h2(own_hi - own_lo, halo, target, src.n_images, cols.tiles_x, cols.wide ? 1 : 2);
     const int sh = L.th + 2 * halo;
     if (sh > max_rows) return fail(PHG_EINVAL, "tile too tall");
-    const size_t smem = b2 ? phg::bp2_smem(sh, direct) : phg::bp_smem(sh);
+    const size_t smem = b2 ? phg::bp2_smem(sh, direct) : phg::bp_smem(sh, direct);
     CUtensorMap map;
     PHG_TRY(encode_map(&map, src, sh, cols.wide ? 64 : 32));
     phg::BpArgs a{};
@@ -411,7 +413,7 @@ int launch_bp(const phg_dev_image& src, const phg_dev_image& dst, int row_base, 
     if (b2)
         PHG_CUDA(phg::launch_bp2_kernel(iters, p.alpha <= 128, cols.wide, direct, map, a, grid, smem, stream));
     else
-        PHG_CUDA(phg::launch_bp_kernel(iters, p.alpha <= 128, cols.wide, map, a, grid, smem, stream));
+        PHG_CUDA(phg::launch_bp_kernel(iters, p.alpha <= 128, cols.wide, direct, map, a, grid, smem, stream));
     ++g_launches;
     return PHG_OK;
 }

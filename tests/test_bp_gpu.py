@@ -189,13 +189,21 @@ def test_beta2_direct_early_exit():
 
 
 def test_beta2_direct_off_switch_same_result():
-    """PHG_NO_BP2_DIRECT=1 keeps the two-buffer T = 1 form; both agree."""
+    """PHG_NO_DIRECT=1 keeps the two-buffer T = 1 form; both agree."""
     code = ("import numpy as np, paper_1306_5390_b200 as P; from oracle import oracle as O;"
             "n=O.inject_sp_noise(O.synth_image(1500,200,5),0.5,0.5,6);"
             "r=P.denoise(P.GrayImage.from_array(n),P.DenoiseParams(beta=2));"
             "i,s=O.denoise(n,20,2); assert np.array_equal(r.image.pixels,i); "
             "assert [(x.flagged,x.replaced) for x in r.stats]==s; print('ok')")
-    env = dict(os.environ, PHG_NO_BP2_DIRECT="1")
+    env = dict(os.environ, PHG_NO_DIRECT="1")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
+@pytest.mark.parametrize("w,h", [(513, 90), (1025, 91), (1993, 181), (3000, 300), (1024, 7)])
+@pytest.mark.parametrize("alpha", [20, 200])
+def test_beta1_direct_single_iteration(w, h, alpha):
+    """beta = 1, k = 1 on wide regions runs the single-buffer DIRECT form
+    (92-row tiles, HBM stores from the sweep and the drain)."""
+    _check(_sp(w, h, w * 7 + h, 0.4), alpha=alpha, k=1)
