@@ -207,3 +207,45 @@ def test_beta1_direct_single_iteration(w, h, alpha):
     """beta = 1, k = 1 on wide regions runs the single-buffer DIRECT form
     (92-row tiles, HBM stores from the sweep and the drain)."""
     _check(_sp(w, h, w * 7 + h, 0.4), alpha=alpha, k=1)
+
+
+@pytest.mark.parametrize("n,w,beta,k", [(1, 31, 1, 5), (3, 481, 1, 5), (1, 300, 2, 5), (3, 200, 2, 1),
+                                        (1, 100, 1, 1)])
+def test_narrow_pairs_store_nothing_past_the_batch(n, w, beta, k):
+    """Narrow tiles pair images (2p, 2p+1); with an odd batch the last CTA
+    has no image 2p+1 and must not store anything for it.  A guard region
+    after the batch in the same allocation stays untouched, and the stats
+    (counters right behind it) stay exact."""
+    import ctypes as C
+    import torch
+    from paper_1306_5390_b200._lib import PhgDevImage, check, lib
+    h = 70
+    pitch = (w + 15) // 16 * 16
+    imgs = np.stack([_sp(w, h, 17 * i + w, 0.3) for i in range(n)])
+    guard = 2 * h * pitch
+    def dev(t):
+        return PhgDevImage(t.data_ptr(), pitch, h * pitch, w, h, n, 0)
+    bufs = []
+    for fill in (0, 0xAB, 0xAB):
+        t = torch.full((n * h * pitch + guard,), fill, dtype=torch.uint8, device="cuda")
+        bufs.append(t)
+    src = bufs[0][: n * h * pitch].view(n, h, pitch)
+    src[:, :, :w] = torch.from_numpy(imgs).cuda()
+    ctr = torch.zeros(2 * k * n + 64, dtype=torch.int64, device="cuda")
+    ctr[2 * k * n:] = 0x5A5A
+    params = P.DenoiseParams(20, beta, k, 3)._c()
+    L = lib()
+    s, d, t = dev(bufs[0]), dev(bufs[1]), dev(bufs[2])
+    check(L.phg_dev_denoise(C.byref(s), C.byref(d), C.byref(t), C.byref(params), C.c_void_p(ctr.data_ptr()),
+                            C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    for b in bufs[1:]:
+        assert bool((b[n * h * pitch:] == 0xAB).all()), "store past the batch"
+    assert bool((ctr[2 * k * n:] == 0x5A5A).all()), "counter store past the batch"
+    out = bufs[1][: n * h * pitch].view(n, h, pitch)[:, :, :w].cpu().numpy()
+    c = ctr[: 2 * k * n].view(n, k, 2).cpu().numpy()
+    for i in range(n):
+        ref_img, ref_stats = O.denoise(imgs[i], 20, beta, k)
+        assert np.array_equal(out[i], ref_img), i
+        got = [tuple(int(x) for x in c[i, j]) for j in range(len(ref_stats))]
+        assert got == ref_stats, i
