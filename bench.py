@@ -354,24 +354,26 @@ class Run:
         return ms, launches, clk.summary()
 
 
-def plan_of(L, params):
-    """The fused launches of one step, as the library plans them (phg_launch_plan)."""
+def plan_of(L, params, width, rows, n_images):
+    """The fused launches of one resident step, as the library plans them
+    (phg_launch_plan) for n_images images of width x rows."""
     buf = (C.c_int * 64)()
-    n = L.phg_launch_plan(C.byref(params), buf, 64)
+    n = L.phg_launch_plan(C.byref(params), width, rows, n_images, buf, 64)
     if n < 0:
         raise RuntimeError(L.phg_last_error().decode())
     return list(buf[:n])
 
 
 def step_roofline(R, src, dst, tmp, counters, params, w, rows, n, beta, k, reps, row_base=0, height=None,
-                  own=None):
-    """The launches of ONE step (the library's launch plan: one T=5 launch for
-    beta=1, five T=1 launches for beta=2), timed back to back on the launching
-    stream with CUDA events; roofline record against the measured HBM peak."""
+                  own=None, plan=None):
+    """The launches of ONE step (default: the library's resident plan -- one
+    T=5 launch for beta=1, five T=1 launches for beta=2 and for beta=1
+    launches >= 160 Mpx), timed back to back on the launching stream with
+    CUDA events; roofline record against the measured HBM peak."""
     torch, L = R.torch, R.L
     height = height or rows
     own_lo, own_hi = own or (0, height)
-    plan = plan_of(L, params)
+    plan = plan or plan_of(L, params, w, own_hi - own_lo, n)
     k = sum(plan)
     bufs = [src, dst, tmp]
 
@@ -543,10 +545,12 @@ def run_bands(R, a):
     from paper_1306_5390_b200._lib import PhgParams
     S, k = a.c5_size, a.k
     beta = 1
-    tmax = L.phg_max_fused_iterations(beta)
+    params = PhgParams(ALPHA, beta, k, 3, 0)
+    # one rank: the resident plan (T = 1 single-buffer launches at this size);
+    # several: the deepest blocking, one halo exchange per launch
+    tmax = max(plan_of(L, params, S, S, 1)) if R.world == 1 else L.phg_max_fused_iterations(beta)
     plan = D.BandPlan(S, S, R.world, R.rank, beta * tmax)
     pitch = (S + 15) // 16 * 16
-    params = PhgParams(ALPHA, beta, k, 3, 0)
     host = torch.empty((plan.rows, S), dtype=torch.uint8, pin_memory=True)
     bufs = [torch.zeros((plan.rows, pitch), dtype=torch.uint8, device=R.dev) for _ in range(3)]
     if a.gen == "device":
@@ -577,9 +581,10 @@ def run_bands(R, a):
     src = dev_image(bufs[0], S, plan.rows, 1)
     dst = dev_image(bufs[1], S, plan.rows, 1)
     tmp = dev_image(bufs[2], S, plan.rows, 1)
-    roof = step_roofline(R, src, dst, tmp, counters, PhgParams(ALPHA, beta, min(k, tmax), 3, 0), S, plan.rows, 1,
-                         beta, min(k, tmax),
-                         max(5, min(a.steps, 10)), row_base=plan.blo, height=S, own=(plan.lo, plan.hi))
+    kr = min(k, 5)  # the launches of one k=5 step (the band plan's launch depth)
+    roof = step_roofline(R, src, dst, tmp, counters, PhgParams(ALPHA, beta, kr, 3, 0), S, plan.rows, 1, beta, kr,
+                         max(5, min(a.steps, 10)), row_base=plan.blo, height=S, own=(plan.lo, plan.hi),
+                         plan=D.chunk_plan(kr, tmax))
     host_out = torch.empty((plan.hi - plan.lo, S), dtype=torch.uint8, pin_memory=True)
 
     if R.world == 1:

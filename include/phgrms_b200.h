@@ -157,12 +157,14 @@ typedef struct phg_dev_image {
  * (temporal blocking depth; 0 if beta has no fused kernel). */
 int phg_max_fused_iterations(int beta);
 
-/* The launches a denoise with these parameters runs: fills iters_per_launch
- * (capacity cap) with the iterations of each fused launch and returns their
- * number (e.g. k = 5: {5} for beta = 1, {1,1,1,1,1} for the beta = 2 default
- * kernel, whose temporal blocking does not pay); negative on error.  With
- * iters_per_launch == NULL only the count is returned. */
-int phg_launch_plan(const phg_params* p, int* iters_per_launch, int cap);
+/* The launches phg_dev_denoise runs for these parameters on n_images images
+ * of width x rows: fills iters_per_launch (capacity cap) with the iterations
+ * of each fused launch and returns their number; negative on error.  E.g.
+ * k = 5: {5} for beta = 1 (temporal blocking), {1,1,1,1,1} for beta = 2
+ * (whose blocking does not pay) and for beta = 1 launches of >= 160 Mpx on
+ * wide regions (single-buffer T = 1 tiles).  With iters_per_launch == NULL
+ * only the count is returned. */
+int phg_launch_plan(const phg_params* p, int width, int rows, int n_images, int* iters_per_launch, int cap);
 
 /* Name of the kernel one fused launch of `iters` iterations runs for these
  * parameters (static string; "" if none).  For reports and profiles. */

@@ -114,7 +114,7 @@ def lib():
         L.phg_finalize_stats.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(PhgPassStats),
                                          C.POINTER(C.c_int)]
         L.phg_max_fused_iterations.argtypes = [C.c_int]
-        L.phg_launch_plan.argtypes = [C.POINTER(PhgParams), C.c_void_p, C.c_int]
+        L.phg_launch_plan.argtypes = [C.POINTER(PhgParams), C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int]
         L.phg_fused_kernel_name.argtypes = [C.POINTER(PhgParams), C.c_int]
         L.phg_fused_kernel_name.restype = C.c_char_p
         L.phg_residual_noise_count.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,

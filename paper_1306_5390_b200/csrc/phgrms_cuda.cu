@@ -687,6 +687,20 @@ std::vector<int> chunk_plan(int k, const phg_params& p, bool deep = false) {
     return c;
 }
 
+// The resident path's plan for images of these dimensions.  beta = 1 on wide
+// regions: large launches run T = 1 in the single-buffer DIRECT form (92-row
+// tiles, 2% halo against 11% for T = 5 at 46 rows); below ~160 Mpx per launch
+// its per-launch tail costs more than that saves.  Measured (k = 5, 30% s&p,
+// tools/tmax_probe.py): 8192^2 T=5 1050 K vs T=1 993 K Mpix-it/s, 16384^2
+// 1144 vs 1174 K, 32768^2 1169 vs 1227 K.
+std::vector<int> resident_plan(const phg_params& p, int width, int64_t pixels) {
+    if (max_fused(p.beta) <= 0) return std::vector<int>(p.max_iterations, 1);
+    static const bool keep = getenv("PHG_TMAX") != nullptr;  // explicit depth cap: tuning runs
+    if (!keep && use_bp(p, 1) && width > 512 && pixels >= (int64_t(160) << 20))
+        return std::vector<int>(p.max_iterations, 1);
+    return chunk_plan(p.max_iterations, p);
+}
+
 // ------------------------------------------------- layout conversion kernels
 // Host images are unpadded ([n][h][w]); the fused kernel needs 16-byte
 // pitched rows (TMA).  Copying through the copy engine with cudaMemcpy2D and
@@ -964,10 +978,10 @@ int phg_set_device(int device) {
 
 int phg_max_fused_iterations(int beta) { return max_fused(beta); }
 
-int phg_launch_plan(const phg_params* p, int* iters_per_launch, int cap) {
+int phg_launch_plan(const phg_params* p, int width, int rows, int n_images, int* iters_per_launch, int cap) {
     PHG_TRY(validate(p));
-    const std::vector<int> plan =
-        max_fused(p->beta) > 0 ? chunk_plan(p->max_iterations, *p) : std::vector<int>(p->max_iterations, 1);
+    if (width < 1 || rows < 1 || n_images < 1) return fail(PHG_EINVAL, "bad image dimensions");
+    const std::vector<int> plan = resident_plan(*p, width, static_cast<int64_t>(width) * rows * n_images);
     if (iters_per_launch) {
         if (cap < static_cast<int>(plan.size())) return fail(PHG_EINVAL, "launch plan capacity too small");
         std::copy(plan.begin(), plan.end(), iters_per_launch);
@@ -1108,7 +1122,8 @@ int phg_dev_denoise(const phg_dev_image* src, const phg_dev_image* dst, const ph
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int k = p->max_iterations;
     PHG_CUDA(cudaMemsetAsync(counters, 0, sizeof(uint64_t) * 2 * k * src->n_images, st));
-    const std::vector<int> plan = max_fused(p->beta) > 0 ? chunk_plan(k, *p) : std::vector<int>(k, 1);
+    const std::vector<int> plan =
+        resident_plan(*p, src->width, static_cast<int64_t>(src->width) * src->rows * src->n_images);
     const int nl = static_cast<int>(plan.size());
     const phg_dev_image* cur = src;
     int it0 = 0;
