@@ -178,8 +178,7 @@ __device__ __forceinline__ uint32_t bp_replace(uint32_t o1, uint32_t k7) {
     const uint32_t dis2 = (ALE ? (d2 | t2) : (d2 & t2)) & kHi;
     const uint32_t f = __popc(dis1 | (dis2 >> 1));
     const uint32_t S = __dp4a(n2 & msb_to_bytes(dis2), n2, __dp4a(n1 & msb_to_bytes(dis1), n1, 0u));
-    const float rcp = f == 8u ? 0.125f : 0.142857149f;  // f in {7, 8}
-    return h2_rms(S, f, rcp);
+    return h2_rms(S, f, rms_rcp<7>(f));  // f in {7, 8}
 }
 
 // DIRECT (T = 1, wide regions, no peer mirrors): one staged buffer; owned

@@ -133,8 +133,7 @@ __device__ __forceinline__ uint32_t bp2_replace(uint32_t o1, uint32_t k7) {
         S = __dp4a(n[i] & msb_to_bytes(dis), n[i], S);
     }
     const uint32_t f = __popc(packed);  // 23 or 24
-    const float rcp = f == 24u ? 0.0416666679f : 0.0434782617f;
-    return h2_rms(S, f, rcp);
+    return h2_rms(S, f, rms_rcp<23>(f));  // f in {23, 24}
 }
 
 template <int T, bool ALE, bool WIDE, bool DIRECT = false>

@@ -168,18 +168,30 @@ __device__ __forceinline__ void h2_pairs_down(const uint32_t (&v)[6], const uint
 // for S < 2^23 and f in {7, 8} (beta = 1) or {23, 24} (beta = 2), rcp_f =
 // fp32(1/f).  r ~ sqrt(S/f): one rounding in rcp_f, one in the product and
 // MUFU.SQRT's own error, together a relative error below 2^-21.  Scaling r by
-// 1 + 2^-20 inside the rounding FFMA lifts it strictly above the exact root
-// and by less than 273 * 2^-19 < 1/2, so n = nearest(r (1 + 2^-20)) is the
-// exact u = floor(sqrt(S/f) + 1/2) or u + 1, and u = n - [n > 0 and
-// (2n-1)^2 f > 4S] (an exact integer test).  Exhaustively checked on the GPU
-// for every S up to 24 * 65025 (tests/test_parity_gpu.py, phg_debug_rms).
+// 1 - 2^-20 inside the rounding FFMA puts it strictly below the exact root x
+// (x > 0) and by less than 273 * 2^-19 < 1/2, so n = nearest(r (1 - 2^-20)) is
+// the exact u = floor(x + 1/2) or u - 1 (and n >= 0), and u = n + [4S >= f
+// (2n+1)^2] (an exact integer test, on the FMA pipe but for one compare).
+// The FFMA's result is 0x4b400000 + n; the constant is carried through to
+// the end (its low byte is 0).  Exhaustively checked on the GPU for every S
+// up to 24 * 65025 (tests/test_parity_gpu.py, phg_debug_rms).
 __device__ __forceinline__ uint32_t h2_rms(uint32_t S, uint32_t f, float rcp_f) {
     const float s = __int_as_float(0x4b000000 | S) - 8388608.0f;  // exact
     float r;
     asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(s * rcp_f));
-    const int n = __float_as_int(fmaf(r, 1.00000095367431640625f, 12582912.0f)) - 0x4b400000;
-    const uint32_t q = 2u * static_cast<uint32_t>(n) - 1u;
-    return static_cast<uint32_t>(n) - ((n > 0 && q * q * f > 4u * S) ? 1u : 0u);
+    const uint32_t nb = __float_as_uint(fmaf(r, 0.99999904632568359375f, 12582912.0f));  // 0x4b400000 + n
+    const uint32_t q = 2u * nb + (1u - 2u * 0x4b400000u);                                // 2n + 1
+    return nb - 0x4b400000u + (q * (q * f) <= 4u * S ? 1u : 0u);
+}
+
+// fp32(1/f) for the two values f takes in a replacement, as one IMAD on the
+// FMA pipe: f in {F0, F0 + 1} = {7, 8} (beta = 1) or {23, 24} (beta = 2)
+template <int F0>
+__device__ __forceinline__ float rms_rcp(uint32_t f) {
+    static_assert(F0 == 7 || F0 == 23, "beta = 1 or 2");
+    constexpr uint32_t b0 = F0 == 7 ? 0x3e124925u : 0x3d321643u;  // fp32(1/F0)
+    constexpr uint32_t b1 = F0 == 7 ? 0x3e000000u : 0x3d2aaaabu;  // fp32(1/(F0 + 1))
+    return __uint_as_float(b0 + static_cast<uint32_t>(F0) * (b0 - b1) - f * (b0 - b1));
 }
 
 __device__ __forceinline__ void sts16(uint32_t addr, uint32_t v) {
@@ -216,8 +228,7 @@ __device__ __forceinline__ uint32_t h2_replace(uint32_t src, int o1, uint32_t k7
     const uint32_t dis2 = (ALE ? (d2 | t2) : (d2 & t2)) & kHi;
     const uint32_t f = __popc(dis1 | (dis2 >> 1));
     const uint32_t S = __dp4a(n2 & msb_to_bytes(dis2), n2, __dp4a(n1 & msb_to_bytes(dis1), n1, 0u));
-    const float rcp = f == 8u ? 0.125f : 0.142857149f;  // f in {7, 8}
-    return h2_rms(S, f, rcp);
+    return h2_rms(S, f, rms_rcp<7>(f));  // f in {7, 8}
 }
 
 template <int T, bool ALE>

@@ -212,8 +212,7 @@ __device__ __forceinline__ uint32_t h2b2_replace(uint32_t src, int o, uint32_t k
         f += __popc(dis);
         S = __dp4a(nb[i] & msb_to_bytes(dis), nb[i], S);
     }
-    const float rcp = f == 24u ? 0.0416666679f : 0.0434782617f;  // f in {23, 24}
-    return h2_rms(S, f, rcp);
+    return h2_rms(S, f, rms_rcp<23>(f));  // f in {23, 24}
 }
 
 template <int T, bool ALE>

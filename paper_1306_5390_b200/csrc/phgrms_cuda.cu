@@ -41,9 +41,11 @@ void set_error(const std::string& msg) { g_error = msg; }
 }  // namespace phg_internal
 
 // phg_debug_rms: the fused kernels' RMS replacement for every S < n.
+// (rcp_f as the kernels derive it, phg::rms_rcp; the host's 1/f must agree)
 __global__ void rms_probe_kernel(uint32_t f, float rcp_f, uint32_t n, uint32_t* out) {
     const uint32_t S = blockIdx.x * blockDim.x + threadIdx.x;
-    if (S < n) out[S] = phg::h2_rms(S, f, rcp_f);
+    const float rk = f < 16 ? phg::rms_rcp<7>(f) : phg::rms_rcp<23>(f);
+    if (S < n) out[S] = rk == rcp_f ? phg::h2_rms(S, f, rk) : 0xffffffffu;
 }
 
 namespace {
