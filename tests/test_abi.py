@@ -134,3 +134,25 @@ def test_sharded_argument_errors_without_gpu():
         pass
     with pytest.raises(P.CudaError):
         P.denoise_sharded(img, P.DenoiseParams(), [0])
+
+
+def test_launch_plan_host_only():
+    """phg_launch_plan is host logic (no device needed): the resident path's
+    launches per parameter set and image size."""
+    L = lib()
+
+    def plan(args, w, h, n, cap=64):
+        buf = (C.c_int * cap)()
+        k = L.phg_launch_plan(C.byref(PhgParams(*args)), w, h, n, buf, cap)
+        return list(buf[:k]) if k >= 0 else k
+
+    assert plan((20, 1, 5, 3, 0), 481, 321, 4096) == [5]          # C4: one T=5 launch
+    assert plan((20, 1, 5, 3, 0), 3840, 2160, 1) == [5]           # C2
+    assert plan((20, 1, 5, 3, 0), 65536, 65536, 1) == [1] * 5     # C5: single-buffer T=1 launches
+    assert plan((20, 1, 12, 3, 0), 481, 321, 1) == [4, 4, 4]
+    assert plan((20, 2, 5, 3, 0), 16384, 16384, 1) == [1] * 5     # C3
+    assert plan((20, 1, 5, 3, 1), 4000, 4000, 1) == [5]           # InBounds: fused_tb_kernel
+    assert plan((20, 4, 3, 3, 0), 100, 100, 1) == [1, 1, 1]       # beta >= 4: scalar kernel
+    assert plan((20, 1, 5, 3, 0), 0, 10, 1) < 0
+    assert plan((20, 1, 5, 3, 0), 481, 321, 1, cap=0) < 0
+    assert L.phg_launch_plan(C.byref(PhgParams(20, 1, 5, 3, 0)), 481, 321, 1, None, 0) == 1
