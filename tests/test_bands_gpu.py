@@ -13,12 +13,15 @@ from paper_1306_5390_b200._lib import PhgParams, lib
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("G,W,H,beta,k,border", [(2, 481, 321, 1, 5, 0), (3, 700, 257, 2, 5, 1),
-                                                 (4, 1000, 200, 1, 7, 0), (8, 520, 400, 1, 5, 1)])
-def test_bands_on_one_device_equal_full_image(G, W, H, beta, k, border):
+@pytest.mark.parametrize("G,W,H,beta,k,border,tmax", [
+    (2, 481, 321, 1, 5, 0, 0), (3, 700, 257, 2, 5, 1, 0), (4, 1000, 200, 1, 7, 0, 0), (8, 520, 400, 1, 5, 1, 0),
+    # T = 1 launches: the single-buffer DIRECT form on wide regions (owned
+    # rows of a band stored straight to HBM), the two-buffer form when narrow
+    (3, 1500, 300, 1, 5, 0, 1), (2, 1100, 200, 2, 4, 0, 1), (2, 481, 321, 1, 3, 0, 1)])
+def test_bands_on_one_device_equal_full_image(G, W, H, beta, k, border, tmax):
     lib().phg_set_device(0)
     img = O.inject_sp_noise(O.synth_image(W, H, G * 7 + W), 0.3, 0.5, 11)
-    tmax = lib().phg_max_fused_iterations(beta)
+    tmax = tmax or lib().phg_max_fused_iterations(beta)
     pitch = (W + 15) // 16 * 16
     params = PhgParams(20, beta, k, 3, border)
     counters = torch.zeros((k, 2), dtype=torch.int64, device="cuda")
