@@ -1543,7 +1543,8 @@ int denoise_rows_pipelined(DeviceState* s, const uint8_t* img, int w, int h, con
 // chunks = not worth pipelining (below 4 MB).  4-32 MB: 3 chunks over 8
 // pieces (C2 4K image e2e: 98 K plain, 118 K pipelined; 2-8 chunks x 4-16
 // pieces measured 109-118 K).  Larger: pieces ~2 MB+ (<= 16), chunks ~8 MB+
-// (<= 8), never shorter than 32 rows.  PHG_ROW_CHUNKS / PHG_ROW_PIECES
+// (<= 12: C3 e2e with 8 / 12 / 16 chunks 175 / 191 / 179-188 K, C5 206 / 212
+// / 210-219 K), never shorter than 32 rows.  PHG_ROW_CHUNKS / PHG_ROW_PIECES
 // override.  Rows already 16-byte pitched (width % 16 == 0) are copied
 // straight into / out of the pitched buffers.
 // `halo` = beta * (iterations of the deepest launch): every chunk must be at
@@ -1552,7 +1553,7 @@ int denoise_rows_pipelined(DeviceState* s, const uint8_t* img, int w, int h, con
 // with their readers).
 void row_plan_for(int w, int h, int halo, int& nchunks, int& npieces) {
     const char* ev = getenv("PHG_ROW_CHUNKS");  // read per call (tuning sweeps)
-    const int env = ev ? std::max(0, std::min(8, atoi(ev))) : -1;
+    const int env = ev ? std::max(0, std::min(kMaxRowChunks, atoi(ev))) : -1;
     const char* pv = getenv("PHG_ROW_PIECES");
     const int64_t bytes = static_cast<int64_t>(w) * h;
     nchunks = npieces = 0;
@@ -1562,7 +1563,7 @@ void row_plan_for(int w, int h, int halo, int& nchunks, int& npieces) {
         nchunks = std::max(1, std::min(3, h / 32));
         npieces = std::max(nchunks, std::min(8, h / 32));
     } else {
-        nchunks = env > 0 ? env : static_cast<int>(std::min<int64_t>(8, bytes >> 23));
+        nchunks = env > 0 ? env : static_cast<int>(std::min<int64_t>(12, bytes >> 23));
         nchunks = std::max(1, std::min(nchunks, h / 32));
         npieces = static_cast<int>(std::max<int64_t>(nchunks, std::min<int64_t>(kMaxRowChunks, bytes >> 21)));
         if (pv) npieces = std::max(1, std::min(kMaxRowChunks, atoi(pv)));
