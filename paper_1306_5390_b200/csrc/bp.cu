@@ -53,4 +53,17 @@ cudaError_t launch_bp_kernel(int T, bool ale, bool wide, bool direct, const CUte
 
 size_t bp_smem(int sh, bool direct) { return static_cast<size_t>(bp_smem_bytes(sh, direct)); }
 
+cudaError_t launch_bp_count_kernel(bool ale, bool wide, const CUtensorMap& map, const BpArgs& a, unsigned grid,
+                                   size_t smem, cudaStream_t stream) {
+    BpFn fn = wide ? (ale ? fused_bp_kernel<1, true, true, false, true> : fused_bp_kernel<1, false, true, false, true>)
+                   : (ale ? fused_bp_kernel<1, true, false, false, true> : fused_bp_kernel<1, false, false, false, true>);
+    const size_t cap = bp_smem(kBpDirectMaxRows, true);
+    if (smem > cap) return cudaErrorInvalidValue;
+    cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cap));
+    if (e != cudaSuccess) return e;
+    fn<<<grid, kBpThreads, smem, stream>>>(map, a);
+    return cudaGetLastError();
+}
+
 }  // namespace phg

@@ -46,6 +46,10 @@ cudaError_t launch_bp_kernel(int T, bool ale, bool wide, bool direct, const CUte
                              unsigned grid, size_t smem, cudaStream_t stream);
 // dynamic shared memory of one CTA staging sh rows
 size_t bp_smem(int sh, bool direct = false);
+// The count-only form (fused_bp_kernel<1, ale, wide, false, true>): pixels
+// with C < card_threshold per image into a.counters[image]; one staged buffer.
+cudaError_t launch_bp_count_kernel(bool ale, bool wide, const CUtensorMap& map, const BpArgs& a, unsigned grid,
+                                   size_t smem, cudaStream_t stream);
 // the beta = 2 kernel (kernel_bp2.cuh), T <= 4; `direct`: the single-buffer
 // T = 1 form that stores straight to HBM (wide regions, no peer mirrors)
 cudaError_t launch_bp2_kernel(int T, bool ale, bool wide, bool direct, const CUtensorMap& map, const BpArgs& a,

@@ -183,11 +183,17 @@ __device__ __forceinline__ uint32_t bp_replace(uint32_t o1, uint32_t k7) {
 
 // DIRECT (T = 1, wide regions, no peer mirrors): one staged buffer; owned
 // rows and replaced pixels are stored straight to HBM (see kernel_bp2.cuh).
-template <int T, bool ALE, bool WIDE, bool DIRECT = false>
+// COUNT (T = 1, one staged buffer, either layout): the sweep alone -- the
+// number of owned pixels with C < card_threshold per image goes to
+// counters[image] (residual_noise_count, metrics.hpp:52-59); nothing is
+// replaced or stored.
+template <int T, bool ALE, bool WIDE, bool DIRECT = false, bool COUNT = false>
 __global__ void __launch_bounds__(kBpThreads, 2)
     fused_bp_kernel(const __grid_constant__ CUtensorMap src_map, const BpArgs a) {
     static_assert(T >= 1 && T <= 8, "halo exceeds the aprons");
     static_assert(!DIRECT || (T == 1 && WIDE), "direct stores: one iteration, wide regions");
+    static_assert(!COUNT || (T == 1 && !DIRECT), "count: one iteration");
+    constexpr bool SINGLE = DIRECT || COUNT;  // one staged buffer
     constexpr int HALO = T;
     constexpr int RP = WIDE ? 1024 : 512;  // staged row pitch of one tile
     constexpr int NH = WIDE ? 1 : 2;       // tiles per CTA
@@ -202,7 +208,7 @@ __global__ void __launch_bounds__(kBpThreads, 2)
     const int lane = tid & 31;
     const int warp = tid >> 5;
     const uint32_t s0 = smem_u32(smem);
-    const uint32_t down_a = s0 + (DIRECT ? 1 : 2) * bufb;  // [warps][32][2] u32 band-edge credits
+    const uint32_t down_a = s0 + (SINGLE ? 1 : 2) * bufb;  // [warps][32][2] u32 band-edge credits
     const uint32_t list_a = down_a + kBpWarps * 32 * 8 + warp * kBpList * 2;  // this warp's u16 list
     const uint32_t half_bytes = static_cast<uint32_t>(sh) * 512u;  // narrow: tile B offset
 
@@ -410,7 +416,8 @@ __global__ void __launch_bounds__(kBpThreads, 2)
                 const uint32_t w = wA | wB | (oA & oB), o = oA | oB;
                 // the unchanged row goes to the destination (candidates are
                 // overwritten by the replacement)
-                if constexpr (DIRECT) {
+                if constexpr (COUNT) {
+                } else if constexpr (DIRECT) {
                     if (rowown(y)) {
                         uint8_t* g = a.dst + gtile + static_cast<int64_t>(y) * a.pitch + px0;
                         if (own0) *reinterpret_cast<uint4*>(g) = make_uint4(X[0], X[1], X[2], X[3]);
@@ -425,7 +432,10 @@ __global__ void __launch_bounds__(kBpThreads, 2)
                     of = o;
                     wf = w;
                 } else {
-                    push(finalize(y, o, w), y);
+                    if constexpr (COUNT)
+                        finalize(y, o, w);
+                    else
+                        push(finalize(y, o, w), y);
                 }
                 oP = s | sw;
                 wP = s & sw;
@@ -456,7 +466,10 @@ __global__ void __launch_bounds__(kBpThreads, 2)
                 oM = lds32a(dn);
                 wM = lds32a(dn + 4);
             }
-            push(finalize(b0, of | oM, wf | wM | (of & oM)), b0);
+            if constexpr (COUNT)
+                finalize(b0, of | oM, wf | wM | (of & oM));
+            else
+                push(finalize(b0, of | oM, wf | wM | (of & oM)), b0);
             if (pending) {
                 __syncwarp();
                 drain(0, pending);
@@ -492,7 +505,7 @@ __global__ void __launch_bounds__(kBpThreads, 2)
 
     // ---- owned output rows: 16-byte coalesced stores (DIRECT: only when
     // the iteration was skipped -- the staged rows are the result)
-    if (!DIRECT || nit == 0) {
+    if (!SINGLE || (DIRECT && nit == 0)) {
         const uint8_t* fin = smem + ((nit & 1) ? bufb : 0);
         constexpr int kChunksRow = RP / 16;
         const int c_lo = a.x_apron / 16;
@@ -514,7 +527,12 @@ __global__ void __launch_bounds__(kBpThreads, 2)
             }
         }
     }
-    if (tid < 4 * T && nit > 0) {
+    if constexpr (COUNT) {
+        if (tid < 2) {
+            const unsigned v = red[0][tid];
+            if (v) atomicAdd(&a.counters[tid ? imgB : imgA], static_cast<unsigned long long>(v));
+        }
+    } else if (tid < 4 * T && nit > 0) {
         const int t = tid >> 2, which = tid & 3;
         const unsigned v = red[t][which];
         const int img = (which & 1) ? imgB : imgA;

@@ -420,6 +420,43 @@ int launch_bp(const phg_dev_image& src, const phg_dev_image& dst, int row_base, 
     return PHG_OK;
 }
 
+// residual_noise_count for beta = 1, card_threshold <= 3 (metrics.hpp:52-59):
+// the packed-bit sweep alone (fused_bp_kernel's COUNT form, single buffer,
+// up to 92-row tiles) -- C < thr is exactly its "flagged" decision.
+int launch_bp_count(const phg_dev_image& src, int alpha, int thr, uint64_t* counts, cudaStream_t stream) {
+    const BpCols cols = bp_cols(src.width);
+    const Launch L = plan_rows_h2(src.rows, 1, phg::kBpDirectMaxRows, src.n_images, cols.tiles_x, cols.wide ? 1 : 2);
+    const int sh = L.th + 2;
+    if (sh > phg::kBpDirectMaxRows) return fail(PHG_EINVAL, "tile too tall");
+    CUtensorMap map;
+    PHG_TRY(encode_map(&map, src, sh, cols.wide ? 64 : 32));
+    phg::BpArgs a{};
+    a.pitch = src.pitch;
+    a.image_stride = src.image_stride;
+    a.width = src.width;
+    a.height = src.rows;
+    a.own_hi = src.rows;
+    a.th = L.th;
+    a.tiles_x = cols.tiles_x;
+    a.tiles_y = L.tiles_y;
+    const int64_t n_tiles = static_cast<int64_t>(src.n_images) * a.tiles_x * a.tiles_y;
+    if (n_tiles > (int64_t(1) << 31) - 2) return fail(PHG_EINVAL, "too many tiles for one launch");
+    a.n_tiles = static_cast<int>(n_tiles);
+    a.x_step = cols.x_step;
+    a.x_apron = cols.x_apron;
+    a.k7 = ((256u - static_cast<uint32_t>(alpha)) & 0x7fu) * 0x01010101u;
+    a.one = 1u;
+    a.sel2 = thr == 2 ? ~0u : 0u;
+    a.enable = thr >= 2 ? ~0u : 0u;
+    a.kcap = 1;
+    a.counters = reinterpret_cast<unsigned long long*>(counts);
+    a.peers = kNoPeers;
+    const unsigned grid = static_cast<unsigned>(cols.wide ? n_tiles : (n_tiles + 1) / 2);
+    PHG_CUDA(phg::launch_bp_count_kernel(alpha <= 128, cols.wide, map, a, grid, phg::bp_smem(sh, true), stream));
+    ++g_launches;
+    return PHG_OK;
+}
+
 // beta = 1 cardinality map (kCardMap) or C < thr count (kCardCount) over
 // whole images (rows = src.rows), fp16 two-tile sweep (kernel_card.cuh).
 int launch_card_h2(const phg_dev_image& src, int alpha, int mode, int thr, int32_t* card, int64_t card_pitch,
@@ -1160,6 +1197,8 @@ int phg_dev_residual_count(const phg_dev_image* src, int alpha, int beta, int ca
     if (card_threshold < 1) return fail(PHG_EINVAL, "card_threshold must be >= 1");
     if (!src || !counts) return fail(PHG_EINVAL, "null argument");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    static const bool no_bp = getenv("PHG_NO_BP") != nullptr;
+    if (beta == 1 && card_threshold <= 3 && !no_bp) return launch_bp_count(*src, alpha, card_threshold, counts, st);
     if (beta == 1 && !getenv("PHG_NO_H2"))
         return launch_card_h2(*src, alpha, phg::kCardCount, card_threshold, nullptr, 0, counts, st);
     // wider windows: scalar map into a stream-ordered temporary, then count

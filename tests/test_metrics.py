@@ -130,3 +130,30 @@ def test_cardinality_map_beta2_staged_vs_oracle():
         assert np.array_equal(got, O.cardinality(img, alpha, 2)), (w, h, alpha)
     assert P.cardmap(G(3, 3, 100), beta=2) == "P2\n3 3\n25\n9 12 9\n12 16 12\n9 12 9\n" or \
         P.cardmap(G(3, 3, 100), beta=2)[:9] == "P2\n3 3\n25"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,w,h", [(1, 481, 321), (3, 481, 321), (2, 300, 95), (1, 1500, 400), (2, 2100, 181),
+                                   (3, 17, 200), (1, 1024, 1)])
+@pytest.mark.parametrize("thr,alpha", [(3, 20), (2, 20), (1, 20), (3, 200)])
+def test_residual_count_packed_bit_batches(n, w, h, thr, alpha):
+    """beta = 1, card_threshold <= 3 runs the packed-bit sweep's count-only
+    form (fused_bp_kernel COUNT, up to 92-row tiles, both column layouts):
+    per-image counts of C < thr over batches, against the oracle's map."""
+    import ctypes as C
+    import torch
+    from paper_1306_5390_b200._lib import PhgDevImage, check, lib
+    pitch = (w + 15) // 16 * 16
+    imgs = np.stack([O.inject_sp_noise(O.synth_image(w, h, 5 * i + w), 0.1 + 0.2 * i, 0.5, i + 1)
+                     for i in range(n)])
+    buf = torch.zeros((n, h, pitch), dtype=torch.uint8, device="cuda")
+    buf[:, :, :w] = torch.from_numpy(imgs).cuda()
+    counts = torch.zeros(n + 4, dtype=torch.int64, device="cuda")
+    im = PhgDevImage(buf.data_ptr(), pitch, h * pitch, w, h, n, 0)
+    check(lib().phg_dev_residual_count(C.byref(im), alpha, 1, thr, C.c_void_p(counts.data_ptr()),
+                                       C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    got = counts.cpu().numpy()
+    for i in range(n):
+        ref = int(np.count_nonzero(O.cardinality(imgs[i], alpha, 1) < thr))
+        assert int(got[i]) == ref, (i, n, w, h, thr, alpha)
+    assert not got[n:].any()
