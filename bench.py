@@ -401,7 +401,7 @@ def step_roofline(R, src, dst, tmp, counters, params, w, rows, n, beta, k, reps,
     names = [L.phg_fused_kernel_name(C.byref(params), T).decode() for T in plan]
     name = names[0] if len(names) == 1 else (f"{len(names)} x {names[0]}" if len(set(names)) == 1
                                              else " + ".join(names))
-    traffic = None
+    traffic, issue = None, None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
@@ -409,12 +409,15 @@ def step_roofline(R, src, dst, tmp, counters, params, w, rows, n, beta, k, reps,
             # the committed capture's launches: same kernels, same algorithmic bytes
             if tj.get("kernel") == name and tj.get("algorithmic_bytes_per_launch") == int(alg_bytes):
                 traffic = tj.get("dram_bytes_per_launch")
+                # what does bound the kernel: the integer pipes (same capture)
+                issue = {k: tj[k] for k in ("alu_pipe_pct", "issue_active_pct", "warp_instr_per_px_it") if k in tj}
         except Exception:
             pass
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
             "kernel": name, "launches_per_step": len(plan), "kernel_ms": round(k_ms, 4),
-            "alg_bytes_per_launch": int(alg_bytes / len(plan)), "alg_bytes_per_step": int(alg_bytes)}
+            "alg_bytes_per_launch": int(alg_bytes / len(plan)), "alg_bytes_per_step": int(alg_bytes),
+            "ncu_pipes": issue}
 
 
 def truncated(ctr):
