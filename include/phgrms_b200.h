@@ -161,7 +161,7 @@ int phg_max_fused_iterations(int beta);
  * of width x rows: fills iters_per_launch (capacity cap) with the iterations
  * of each fused launch and returns their number; negative on error.  E.g.
  * k = 5: {5} for beta = 1 (temporal blocking), {1,1,1,1,1} for beta = 2
- * (whose blocking does not pay) and for beta = 1 launches of >= 160 Mpx on
+ * (whose blocking does not pay) and for beta = 1 launches of >= 128 Mpx on
  * wide regions (single-buffer T = 1 tiles).  With iters_per_launch == NULL
  * only the count is returned. */
 int phg_launch_plan(const phg_params* p, int width, int rows, int n_images, int* iters_per_launch, int cap);

@@ -728,14 +728,15 @@ std::vector<int> chunk_plan(int k, const phg_params& p, bool deep = false) {
 
 // The resident path's plan for images of these dimensions.  beta = 1 on wide
 // regions: large launches run T = 1 in the single-buffer DIRECT form (92-row
-// tiles, 2% halo against 11% for T = 5 at 46 rows); below ~160 Mpx per launch
+// tiles, 2% halo against 11% for T = 5 at 46 rows); below ~128 Mpx per launch
 // its per-launch tail costs more than that saves.  Measured (k = 5, 30% s&p,
-// tools/tmax_probe.py): 8192^2 T=5 1050 K vs T=1 993 K Mpix-it/s, 16384^2
-// 1144 vs 1174 K, 32768^2 1169 vs 1227 K.
+// tools/tmax_probe.py, T=5 vs T=1 Mpix-it/s): 8192^2 1059 vs 1006 K, 10240^2
+// 1097 vs 1085 K, 12288^2 1119 vs 1133 K, 16384^2 1156 vs 1197 K, 32768^2
+// 1169 vs 1227 K.
 std::vector<int> resident_plan(const phg_params& p, int width, int64_t pixels) {
     if (max_fused(p.beta) <= 0) return std::vector<int>(p.max_iterations, 1);
     static const bool keep = getenv("PHG_TMAX") != nullptr;  // explicit depth cap: tuning runs
-    if (!keep && use_bp(p, 1) && width > 512 && pixels >= (int64_t(160) << 20))
+    if (!keep && use_bp(p, 1) && width > 512 && pixels >= (int64_t(128) << 20))
         return std::vector<int>(p.max_iterations, 1);
     return chunk_plan(p.max_iterations, p);
 }
