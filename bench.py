@@ -69,8 +69,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c4", choices=["c4", "c2", "c1", "c3", "c5"])
-    ap.add_argument("--k", type=int, default=5, help="iterations (BASELINE: 5; c5 with k > 5 exchanges halos "
-                                                     "between launches inside the step)")
+    ap.add_argument("--k", type=int, default=5, help="iterations (BASELINE: 5; c5 exchanges 1-row halos between "
+                                                     "its T=1 launches inside the step)")
     ap.add_argument("--c5-size", type=int, default=65536, help="c5 image side (parity runs use less)")
     ap.add_argument("--gen", default="reference", choices=["reference", "device"],
                     help="c5 input: the reference generators per 4096^2 tile on the host, or the on-device "
@@ -549,9 +549,10 @@ def run_bands(R, a):
     S, k = a.c5_size, a.k
     beta = 1
     params = PhgParams(ALPHA, beta, k, 3, 0)
-    # one rank: the resident plan (T = 1 single-buffer launches at this size);
-    # several: the deepest blocking, one halo exchange per launch
-    tmax = max(plan_of(L, params, S, S, 1)) if R.world == 1 else L.phg_max_fused_iterations(beta)
+    # the library's resident plan for one rank's band (T = 1 single-buffer
+    # launches from 128 Mpx per launch: 4.3 Gpx / N for N <= 32): one 1-row
+    # halo exchange after every launch but the last, inside the step
+    tmax = max(plan_of(L, params, S, max(1, S // R.world), 1))
     plan = D.BandPlan(S, S, R.world, R.rank, beta * tmax)
     pitch = (S + 15) // 16 * 16
     host = torch.empty((plan.rows, S), dtype=torch.uint8, pin_memory=True)
