@@ -70,6 +70,9 @@ def _bands_worker(rank, world, port, case):
     (2, (64, 50, 0.5, 2, 20, 2, 5, 3, 1, 2)),
     (3, (81, 45, 0.2, 3, 30, 1, 7, 3, 0, 3)),
     (4, (40, 48, 0.6, 4, 20, 1, 5, 2, 1, 2)),
+    # T = 1 launches (the C5 bench plan): a 1-row halo exchange after every
+    # launch but the last
+    (3, (70, 60, 0.3, 5, 20, 1, 5, 3, 0, 1)),
 ])
 def test_row_bands_over_gloo_equal_full_image(world, case):
     mp.spawn(_bands_worker, args=(world, _free_port(), case), nprocs=world, join=True)
