@@ -24,16 +24,21 @@
 //     registers;
 //   - the 8 credits of a pixel are reduced to (o, w) = (>= 1 similar,
 //     >= 2 similar) with 3-input majority / or LOP3s: 32 pixels per op.
-//   Candidates are then a 32-bit word per strip row, stored in shared memory.
-// Replacement: each warp owns a band of rows; after the sweep its lanes split
-// the band's candidates evenly (a warp scan of the per-lane counts, each lane
-// takes a contiguous range of ceil(n/32)) and compute the exact RMS of the
-// dissimilar cells (byte-SIMD masks + IDP.4A sums, h2_rms).
+// Replacement: each warp owns a band of rows.  A finalized row's replaced
+// pixels (one 32-bit word per lane) are pushed into the warp's u16 list of
+// buffer offsets (a warp scan of the per-lane counts, then a bfind loop,
+// three items per trip); whenever a round of 96 is waiting, every lane
+// replaces three: the exact RMS of the dissimilar cells of the 3x3 window
+// (byte-SIMD masks + IDP.4A sums, h2_rms).
 //
 // Band boundaries: a warp's first band row lacks the credits of the pairs with
-// the row above, which the warp above computes as the last step of its band;
-// it parks them in shared memory and the first row is finished after the
-// barrier that ends the sweep (warp 0 computes its own from the row above).
+// the row above, which the warp above computes as the last step of its band
+// and hands over in shared memory through a pairwise named barrier (warp 0
+// computes its own from the row above).  Consecutive iterations synchronise
+// only neighbouring warps when every band holds >= 3 rows.
+//
+// DIRECT / COUNT forms (T = 1, one staged buffer, up to 92-row tiles): see
+// the template below.
 //
 // Tiles.  Narrow images (width <= 512): a CTA holds two consecutive tiles
 // (image, row tile) side by side, one per half-warp (lanes 0-15 / 16-31),
