@@ -1686,11 +1686,14 @@ int phg_denoise_batch(const uint8_t* imgs, int n, int w, int h, const phg_params
     // Chunked pipeline over three streams: contiguous H2D of chunk i+1 and
     // D2H of chunk i-1 overlap the kernels of chunk i (host buffers should
     // be pinned for the copies to be asynchronous).
+    // 8 chunks; 16 from 1024 images (C4, 4096 x 481x321, e2e over 5
+    // interleaved runs: 8 chunks 210.9 K, 16 chunks 216.1 K Mpix-it/s; 12, 20
+    // and 24 measured lower, 32 no better)
     static const int chunks_env = [] {
         const char* e = getenv("PHG_BATCH_CHUNKS");
-        return e ? std::max(1, std::min(256, atoi(e))) : 8;
+        return e ? std::max(1, std::min(256, atoi(e))) : 0;
     }();
-    const int nchunks = std::min(n, n >= 64 ? chunks_env : 1);
+    const int nchunks = std::min(n, n >= 64 ? (chunks_env ? chunks_env : (n >= 1024 ? 16 : 8)) : 1);
     const int per = (n + nchunks - 1) / nchunks;
     const int64_t pitch = round_up(w, 16);
     const int64_t img_bytes = static_cast<int64_t>(w) * h, img_pitched = pitch * h;
