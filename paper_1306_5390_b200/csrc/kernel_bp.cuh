@@ -60,7 +60,7 @@
 
 namespace phg {
 
-constexpr int kBpWarps = 8;
+constexpr int kBpWarps = 8;  // (band splits divide by 8 as a shift)
 constexpr int kBpThreads = 32 * kBpWarps;
 constexpr int kBpPad = 128;        // dynamic smem starts with a pad (window reads at region column -1)
 #ifndef PHG_BP_DRAIN
@@ -300,7 +300,9 @@ __global__ void __launch_bounds__(kBpThreads, 2)
         const uint32_t dst = s0 + ((t & 1) ? 0 : bufb);
         const int lo = t + 1, n = sh - 2 - 2 * t;  // computed rows [lo, lo + n)
         const int nb = min(kBpWarps, n);
-        const int b0 = lo + n * warp / nb, b1 = lo + n * (warp + 1) / nb;
+        // (nb == 8 whenever n >= 8: a shift instead of two integer divisions)
+        const int b0 = lo + (nb == kBpWarps ? (n * warp) >> 3 : n * warp / nb);
+        const int b1 = lo + (nb == kBpWarps ? (n * (warp + 1)) >> 3 : n * (warp + 1) / nb);
         const bool active = warp < nb;
         unsigned fl = 0, rp = 0;  // owned flagged / replaced (this lane's strip)
         uint32_t of = 0, wf = 0;  // the band's first row before its upper credits

@@ -243,7 +243,9 @@ __global__ void __launch_bounds__(kBpThreads, 2)
         const int n = hi - lo;
         // steps [lo, hi + 2) split over the warps, at least two per warp
         const int nb = min(kBpWarps, (n + 2) / 2);
-        const int b0 = lo + (n + 2) * warp / nb, b1 = lo + (n + 2) * (warp + 1) / nb;
+        // (nb == 8 whenever n + 2 >= 16: a shift instead of two integer divisions)
+        const int b0 = lo + (nb == kBpWarps ? ((n + 2) * warp) >> 3 : (n + 2) * warp / nb);
+        const int b1 = lo + (nb == kBpWarps ? ((n + 2) * (warp + 1)) >> 3 : (n + 2) * (warp + 1) / nb);
         const bool active = warp < nb;
         const bool last = warp == nb - 1;
         unsigned fl = 0, rp = 0;
