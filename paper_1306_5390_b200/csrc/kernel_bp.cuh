@@ -170,10 +170,9 @@ __device__ __forceinline__ void bp_load(uint32_t a, uint32_t (&X)[8], uint32_t (
 template <bool ALE, int RP>
 __device__ __forceinline__ uint32_t bp_replace(uint32_t o1, uint32_t k7) {
     const uint32_t b4 = o1 & ~3u;
-    const uint32_t sel = 0x0210u + (o1 & 3u) * 0x0111u;  // bytes s, s+1, s+2
-    uint32_t R[3];
+    uint32_t R[3];  // bytes 0..2: the window row
 #pragma unroll
-    for (int r = 0; r < 3; ++r) R[r] = prmt(lds32a(b4 + r * RP), lds32a(b4 + r * RP + 4), sel);
+    for (int r = 0; r < 3; ++r) R[r] = prmt_f4e(lds32a(b4 + r * RP), lds32a(b4 + r * RP + 4), o1);
     const uint32_t n1 = prmt(R[0], R[1], 0x4210);  // t0 t1 t2 m0
     const uint32_t n2 = prmt(R[1], R[2], 0x6542);  // m2 b0 b1 b2
     const uint32_t p4 = prmt(R[1], 0, 0x1111);     // centre x4

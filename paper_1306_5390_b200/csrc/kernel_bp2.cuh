@@ -107,13 +107,12 @@ __device__ __forceinline__ void bp2_load(uint32_t a, uint32_t (&X)[8], uint32_t 
 template <bool ALE, int RP>
 __device__ __forceinline__ uint32_t bp2_replace(uint32_t o1, uint32_t k7) {
     const uint32_t b4 = o1 & ~3u;
-    const uint32_t s8 = (o1 & 3u) * 8u;
     uint32_t L[5], H[5];  // bytes 0..3 and byte 4 of each window row
 #pragma unroll
     for (int r = 0; r < 5; ++r) {
         const uint32_t w0 = lds32a(b4 + r * RP), w1 = lds32a(b4 + r * RP + 4);
-        L[r] = __funnelshift_r(w0, w1, s8);
-        H[r] = __funnelshift_r(w1, 0u, s8);  // byte 4 of the window row in the low byte
+        L[r] = prmt_f4e(w0, w1, o1);
+        H[r] = prmt_f4e(w1, 0u, o1);  // byte 4 of the window row in the low byte
     }
     const uint32_t c4 = prmt(L[2], 0, 0x2222);  // centre x4
     uint32_t n[6];

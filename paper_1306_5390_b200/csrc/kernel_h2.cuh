@@ -114,6 +114,13 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
     asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
     return r;
 }
+// bytes s .. s+3 of the 8-byte {b:a} with s = sel & 3 (PRMT's forward 4-extract
+// mode: a byte funnel shift whose selector is the byte address itself)
+__device__ __forceinline__ uint32_t prmt_f4e(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t r;
+    asm("prmt.b32.f4e %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+    return r;
+}
 __device__ __forceinline__ uint32_t f2h(float f) {
     return static_cast<uint32_t>(__half_as_ushort(__float2half_rn(f)));
 }
