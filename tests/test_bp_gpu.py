@@ -249,3 +249,21 @@ def test_narrow_pairs_store_nothing_past_the_batch(n, w, beta, k):
         assert np.array_equal(out[i], ref_img), i
         got = [tuple(int(x) for x in c[i, j]) for j in range(len(ref_stats))]
         assert got == ref_stats, i
+
+
+def test_random_shapes_and_plans():
+    """Random widths (both layouts), heights, densities, alpha, thresholds and
+    k (k = 1: the single-buffer DIRECT form on wide regions; k = 6, 7:
+    two-launch plans) against the oracle, beta 1 and 2."""
+    rng = np.random.default_rng(20261019)
+    for _ in range(40):
+        w, h = int(rng.integers(1, 2600)), int(rng.integers(1, 220))
+        beta = int(rng.integers(1, 3))
+        k = int(rng.choice([1, 2, 3, 6, 7]))
+        thr = int(rng.integers(1, 4))
+        alpha = int(rng.choice([5, 20, 60, 128, 129, 240]))
+        img = _sp(w, h, int(rng.integers(0, 1 << 20)), float(rng.uniform(0.05, 0.7)))
+        res = P.denoise(P.GrayImage.from_array(img), P.DenoiseParams(alpha, beta, k, thr))
+        ref_img, ref_stats = O.denoise(img, alpha, beta, k, thr, 0)
+        assert np.array_equal(res.image.pixels, ref_img), (w, h, beta, k, thr, alpha)
+        assert [(s.flagged, s.replaced) for s in res.stats] == ref_stats, (w, h, beta, k, thr, alpha)
